@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the B200 Monte-Carlo sample-solve path.
+
+Metric (BASELINE.json): MC samples solved per second (fp64 batched PCG) on
+B200, with the PCG kernel's roofline fraction and the mean PCG iteration count.
+One "step" = one pass of the hot path over one batch: assign (b) -> bucket (c)
+-> realise (a) -> batched PCG (d) -> per-centroid reduction, i.e. the
+reference's run_campaign_with (proj/src/driver.cpp:193-281) minus setup.
+
+Workload: configs[1] of BASELINE.json (C2: 1-D P1 FEM with 4095 unknowns,
+2^17 samples per GPU, KL n_KL=100 -> 73 modes kept by the reference cutoff,
+k-means d=8/P=64 from 5e4 pilot draws, exact tridiagonal Cholesky centroid
+preconditioners, PCG rtol 1e-8). Inputs are the seeded counter-RNG draws
+(synthetic by definition; there is no dataset).
+
+* value: inputs resident in HBM, CUDA events on the context's stream, max over
+  ranks; weak scaling (each rank solves its own 2^17 samples, indices
+  [rank*B, (rank+1)*B) of the same stream), one int64 all-reduce of the
+  per-centroid statistics per step when N > 1.
+* e2e: the same step through the host-buffer C-ABI call vqpc_run_campaign
+  (pinned host xi copied in, per-sample results copied out, every step).
+* roofline: the PCG kernel's algorithmic fp64 flops (31 n per iteration,
+  SURVEY §8d) / its event-timed duration, against the fp64 FMA-pipe peak
+  measured on this device by vqpc_fp64_peak.
+* cpu_baseline: the CPU oracle's run_campaign_with (oracle/, all host
+  threads) on a bounded sample of the same workload, rank 0 at N = 1.
+* --impl reference: the reference's CPU path (the oracle port, see DESIGN.md:
+  the reference itself cannot be built here — Eigen/Boost absent — and has no
+  1-D model), timed on bounded samples, same metric/unit/config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MC samples solved/sec (fp64 batched PCG) at 1 B200; % roofline; mean PCG iters"
+UNIT = "samples/s"
+FLOPS_PER_ROW_ITER = 31  # 1-D PCG iteration = 31 n flops
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--n", type=int, default=0, help="samples per GPU (default: the config's)")
+    ap.add_argument("--cpu-samples", type=int, default=0, help="CPU baseline sample size")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def workload(cfg, B, K):
+    return {"workload": f"{cfg['name']}: 1-D P1 FEM, {cfg['mesh_resolution'] - 1} unknowns, "
+                        f"{B} samples/GPU, KL {K} modes (n_KL={cfg['n_kl']}), {cfg['quantizer']['method']} "
+                        f"d={cfg['m']} P={cfg['quantizer']['P']}, tridiagonal-Cholesky PCG rtol {cfg['eps']:g}",
+            "samples_per_gpu": B, "unknowns": cfg["mesh_resolution"] - 1, "n_kl": K, "d": cfg["m"],
+            "P": cfg["quantizer"]["P"], "eps": cfg["eps"],
+            "l2": "inputs larger than L2 (kappa %.1f GB written and read per step)" % (B * cfg["mesh_resolution"] * 8 / 1e9)}
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(cfg, arts, n_cpu, index0=0):
+    """The CPU oracle's run_campaign_with on a bounded sample (all host threads)."""
+    import oracle
+    basis, cb = arts["basis"], arts["codebook"]
+    K = basis["eigenvalues"].size
+    xi = oracle.draw_standard_normal(n_cpu, K, cfg["master_seed"], index0)
+    ocb = oracle.Codebook(cb["method"], cb["map"], cb["lambdas"], cb["centroids"], cb.get("latent"))
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    res = oracle.run_campaign(cfg["dim"], cfg["mesh_resolution"], cfg["precond"], ocb, basis["eigenvalues"],
+                              basis["eigenvectors"], xi, cfg["eps"], threads=threads)
+    dt = time.perf_counter() - t0
+    st = res["status"]
+    return dict(value=n_cpu / dt, unit=UNIT, cores=threads, kind="port", seconds=dt,
+                sample=f"first {n_cpu} realisations (indices {index0}..{index0 + n_cpu - 1}) of the {cfg['name']} "
+                       f"stream, run_campaign_with restated in oracle/ (threads={threads}, groups by centroid)",
+                mean_pcg_iters=float(res["iterations"][st == 0].mean()) if (st == 0).any() else 0.0,
+                stage_seconds=res["timings"])
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2403_07824_b200 import campaign
+    cfg = campaign.CONFIGS[args.config]
+    import oracle
+    oracle.build()
+    arts = campaign.prepare_campaign(cfg, kmeans_fn=oracle.kmeans, draw_fn=oracle.draw_standard_normal)
+    K = arts["basis"]["eigenvalues"].size
+    n_step = args.cpu_samples or (256 if cfg["mesh_resolution"] >= 4096 else 1024)
+    times = []
+    last = None
+    for s in range(args.warmup + args.steps):
+        r = cpu_baseline(cfg, arts, n_step, index0=s * n_step)
+        if s >= args.warmup:
+            times.append(r["seconds"])
+            last = r
+    t = float(np.sum(times))
+    value = n_step * args.steps / t
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded counter-RNG xi; no dataset exists for this path)",
+            "config": workload(cfg, n_step, K),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"], "kind": "port",
+                             "sample": f"{n_step} realisations per step, {args.steps} timed steps: " + last["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "mean_pcg_iters": last["mean_pcg_iters"]}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    from paper_2403_07824_b200 import campaign, lib
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = campaign.CONFIGS[args.config]
+    if rank == 0 or world == 1:
+        arts = campaign.prepare_campaign(cfg)  # GPU-assisted kmeans on cache miss
+    if dist:
+        dist.barrier()
+        if rank != 0:
+            arts = campaign.prepare_campaign(cfg)
+    basis, cb = arts["basis"], arts["codebook"]
+    K = basis["eigenvalues"].size
+    B = args.n or cfg["n_realizations"]
+    P = cb["P"]
+    # this rank's inputs: realisations [rank*B, (rank+1)*B) of the master stream
+    xi_np = lib.draw_standard_normal(B, K, cfg["master_seed"], index0=rank * B)
+    xi_pin = torch.from_numpy(xi_np).pin_memory()
+    d_xi = xi_pin.to(dev)
+    d_lab = torch.empty(B, dtype=torch.int32, device=dev)
+    d_it = torch.empty(B, dtype=torch.int32, device=dev)
+    d_rel = torch.empty(B, dtype=torch.float64, device=dev)
+    d_st = torch.empty(B, dtype=torch.uint8, device=dev)
+    d_stats = torch.empty(4 * P + 4, dtype=torch.int64, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    ctx = campaign.make_context(cfg, arts, device=local_rank)
+    ctx.set_stream(stream.cuda_stream)
+
+    def step():
+        ctx.run_campaign_device(d_xi.data_ptr(), B, K, cfg["eps"], d_lab.data_ptr(), d_it.data_ptr(),
+                                d_rel.data_ptr(), d_st.data_ptr(), d_stats.data_ptr(), d_stats.data_ptr() + 8 * 4 * P,
+                                chunk=cfg.get("chunk", 0))
+        if dist:
+            with torch.cuda.stream(stream):
+                dist.all_reduce(d_stats)  # per-centroid n_p / sum_J / converged stats (driver.cpp:241-258)
+
+    for _ in range(args.warmup):
+        step()
+    ctx.synchronize()
+    ctx.profile(True)
+    ctx.profile_read(reset=True)
+    launches0 = ctx.launches
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local_rank) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    launches = ctx.launches - launches0
+    prof = ctx.profile_read(reset=True)
+    ctx.profile(False)
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * B * args.steps / (ms_max / 1e3)
+
+    # per-step solve statistics (identical every step)
+    st = d_st.cpu().numpy()
+    it = d_it.cpu().numpy()
+    total_iters = int(it.astype(np.int64).sum())
+    conv = st == 0
+    n = cfg["mesh_resolution"] - 1
+
+    # roofline of the dominant kernel (pcg): algorithmic fp64 flops / event time
+    pcg = prof["pcg"]
+    pcg_ms = pcg["ms"] / max(pcg["launches"], 1)
+    launches_per_step = max(pcg["launches"] // args.steps, 1)
+    flops_per_launch = FLOPS_PER_ROW_ITER * n * total_iters / launches_per_step
+    achieved = flops_per_launch / (pcg_ms / 1e3) / 1e12
+    peak = lib.fp64_peak(local_rank)
+    traffic = None
+    summ = os.path.join(ROOT, "profiles", "pcg_ncu_summary.json")
+    if os.path.exists(summ):
+        try:
+            traffic = json.load(open(summ)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    step_ms = ms_max / args.steps
+    kernels = {k: {"ms_per_step": v["ms"] / args.steps, "share": (v["ms"] / args.steps) / step_ms if step_ms else 0,
+                   "launches": v["launches"]} for k, v in prof.items()}
+
+    # e2e through the host-buffer C-ABI entry point (copies inside the timed region)
+    e2e_times = []
+    for s in range(args.steps + 1):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        res = ctx.run_campaign(xi_pin.numpy(), cfg["eps"], chunk=cfg.get("chunk", 0))
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_t = float(np.sum(e2e_times[1:]))  # first call warms the host-side buffers
+    e2e_val = world * B * args.steps / e2e_t
+    if dist:
+        te = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_val = world * B * args.steps / float(te.item())
+    h2d = B * K * 8
+    d2h = B * (4 + 4 + 8 + 1) + 8 * (4 * P + 4)
+    assert np.array_equal(res["iterations"], it) and np.array_equal(res["status"], st)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        n_cpu = args.cpu_samples or (512 if cfg["mesh_resolution"] >= 4096 else 2048)
+        cpu = cpu_baseline(cfg, arts, n_cpu)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded counter-RNG xi; no dataset exists for this path)",
+                "config": workload(cfg, B, K),
+                "mean_pcg_iters": float(it[conv].mean()) if conv.any() else 0.0,
+                "status_counts": {lib.STATUS[k]: int((st == k).sum()) for k in np.unique(st)},
+                "total_pcg_iterations_per_gpu_step": total_iters,
+                "roofline": {"kernel": "pcg1d", "bound": "fp64", "achieved": achieved, "peak": peak,
+                             "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": traffic,
+                             "peak_source": "measured on this device: vqpc_fp64_peak DFMA-throughput probe "
+                                            "(MEASURED_PEAKS.json has no fp64 entry)",
+                             "algorithmic": f"{FLOPS_PER_ROW_ITER} n flops per PCG iteration x sum of J over the batch",
+                             "ms_per_launch": pcg_ms},
+                "kernels": kernels,
+                "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "gpu_launches": int(launches),
+                "clocks": clk.summary(),
+                "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

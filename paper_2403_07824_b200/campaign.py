@@ -1,0 +1,203 @@
+"""Campaign driver on the GPU path — mirrors proj/include/vqp/driver.hpp.
+
+* ``CONFIGS``: the five BASELINE.json configurations (C1..C5) in the
+  reference's CampaignConfig vocabulary (driver.hpp:17-49) plus the fields the
+  reference lacks: ``dim``, ``kl_cutoff``, ``precond: "ic0"``,
+  ``quantizer.method: "sign_grid"``, ``chunk``, ``solve_subset``.
+* ``prepare_campaign`` (driver.cpp:166-187): KL basis, pilot draws and codebook,
+  cached as ``.klb``/``.qnt`` artifacts (artifacts.cpp formats).
+* ``draw_realizations`` (driver.cpp:189-191).
+* ``run_campaign_with`` (driver.cpp:193-281): the hot path through the C ABI,
+  returning the reference's SimulationReport fields.
+"""
+from __future__ import annotations
+
+import copy
+import hashlib
+import json
+import os
+
+import numpy as np
+
+from . import artifacts as art
+from . import klbasis
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CACHE = os.environ.get("VQP_ARTIFACTS", os.path.join(ROOT, "artifacts"))
+
+_BASE = dict(sigma2=1.0, ell=0.1, eps=1e-8, master_seed=0, precond="cholesky", kl_cutoff=True, chunk=0,
+             quantizer=dict(method="kmeans", map="scale", seed=1, init_seed=1, max_iter=200, rel_tol=1e-6))
+
+
+def _cfg(**kw):
+    c = copy.deepcopy(_BASE)
+    q = kw.pop("quantizer", {})
+    c.update(kw)
+    c["quantizer"].update(q)
+    return c
+
+
+CONFIGS = {
+    # C1: BASELINE.json configs[0] — the reference-scale CPU-runnable case
+    "C1": _cfg(name="C1", dim=1, mesh_resolution=1024, sigma2=1.0, ell=0.1, n_kl=50, m=4, n_realizations=4096,
+               quantizer=dict(P=16, ns=10_000)),
+    # C2: configs[1] — the headline (bench) workload
+    "C2": _cfg(name="C2", dim=1, mesh_resolution=4096, sigma2=1.0, ell=0.05, n_kl=100, m=8, n_realizations=1 << 17,
+               quantizer=dict(P=64, ns=50_000)),
+    # C3: deterministic sign grid, P = 2^10
+    "C3": _cfg(name="C3", dim=1, mesh_resolution=2048, sigma2=2.0, ell=0.1, n_kl=100, m=10, n_realizations=1 << 16,
+               quantizer=dict(method="sign_grid", P=1024, ns=0)),
+    # C4: 2-D 256 x 256, IC(0)
+    "C4": _cfg(name="C4", dim=2, mesh_resolution=256, sigma2=1.0, ell=0.2, n_kl=100, m=10, n_realizations=8192,
+               precond="ic0", quantizer=dict(P=32, ns=20_000)),
+    # C5: realisation + assignment stress test; PCG on a 2^16 subset; no KL cutoff
+    "C5": _cfg(name="C5", dim=1, mesh_resolution=8192, sigma2=1.0, ell=0.1, n_kl=256, m=64, n_realizations=1 << 20,
+               kl_cutoff=False, chunk=1 << 14, solve_subset=1 << 16, quantizer=dict(P=4096, ns=1 << 18)),
+}
+
+
+def unknowns(cfg):
+    r = cfg["mesh_resolution"]
+    return r - 1 if cfg["dim"] == 1 else (r - 1) ** 2
+
+
+def n_nodes(cfg):
+    r = cfg["mesh_resolution"]
+    return r if cfg["dim"] == 1 else (r + 1) ** 2
+
+
+def scaled(cfg, n_realizations=None, ns=None, **kw):
+    """A copy of ``cfg`` with fewer realisations / pilot samples (tests)."""
+    c = copy.deepcopy(cfg)
+    if n_realizations is not None:
+        c["n_realizations"] = n_realizations
+    if ns is not None:
+        c["quantizer"]["ns"] = ns
+    c.update(kw)
+    return c
+
+
+def _key(cfg, what):
+    if what == "basis":
+        sub = {k: cfg[k] for k in ("dim", "mesh_resolution", "sigma2", "ell", "n_kl", "kl_cutoff")}
+    else:
+        sub = {k: cfg[k] for k in ("dim", "mesh_resolution", "sigma2", "ell", "n_kl", "kl_cutoff", "m")}
+        sub["quantizer"] = cfg["quantizer"]
+    return hashlib.sha1(json.dumps(sub, sort_keys=True).encode()).hexdigest()[:16]
+
+
+def build_basis(cfg):
+    if cfg["dim"] == 1:
+        return klbasis.build_kl_basis_1d(cfg["mesh_resolution"], cfg["sigma2"], cfg["ell"], cfg["n_kl"],
+                                         cfg["kl_cutoff"])
+    return klbasis.build_kl_basis_2d(cfg["mesh_resolution"], cfg["sigma2"], cfg["ell"], cfg["n_kl"], cfg["kl_cutoff"])
+
+
+def load_or_build_basis(cfg, cache=True):
+    path = os.path.join(CACHE, f"basis_{_key(cfg, 'basis')}.klb")
+    if cache and os.path.exists(path):
+        return art.load_kl_basis(path)
+    b = build_basis(cfg)
+    if cache:
+        os.makedirs(CACHE, exist_ok=True)
+        art.save_kl_basis(path + ".tmp", b)
+        os.replace(path + ".tmp", path)
+        b = art.load_kl_basis(path)
+    return b
+
+
+def build_codebook(cfg, basis, kmeans_fn=None, draw_fn=None):
+    """build_codebook (driver.cpp:128-138). kmeans_fn(samples, lambdas, P, map=,
+    init_seed=, max_iter=, rel_tol=) -> (centroids, history) and
+    draw_fn(n, m, seed) default to the GPU-assisted ``lib.kmeans`` and the host
+    ``lib.draw_standard_normal``."""
+    q = cfg["quantizer"]
+    m = cfg["m"]
+    if m > basis["eigenvalues"].size:
+        raise ValueError("mode-count-out-of-range")
+    lam = np.ascontiguousarray(basis["eigenvalues"][:m])
+    root = np.sqrt(lam)
+    if q["method"] == "sign_grid":
+        latent = art.sign_grid_sites(m)
+        return dict(m=m, P=latent.shape[0], map=q["map"], method="sign_grid", seed=0, lambdas=lam,
+                    centroids=latent * root[None, :], latent=latent)
+    if q["method"] != "kmeans":
+        raise ValueError("only kmeans / sign_grid codebooks are configured")
+    if kmeans_fn is None or draw_fn is None:
+        from . import lib
+        kmeans_fn = kmeans_fn or lib.kmeans
+        draw_fn = draw_fn or lib.draw_standard_normal
+    pilot = draw_fn(q["ns"], m, q["seed"])
+    cen, _ = kmeans_fn(pilot, lam, q["P"], map=q["map"], init_seed=q["init_seed"], max_iter=q["max_iter"],
+                       rel_tol=q["rel_tol"])
+    return dict(m=m, P=q["P"], map=q["map"], method="kmeans", seed=q["init_seed"], lambdas=lam, centroids=cen,
+                latent=None)
+
+
+def load_or_build_codebook(cfg, basis, cache=True, kmeans_fn=None, draw_fn=None):
+    path = os.path.join(CACHE, f"codebook_{_key(cfg, 'codebook')}.qnt")
+    if cache and os.path.exists(path):
+        return art.load_codebook(path)
+    cb = build_codebook(cfg, basis, kmeans_fn, draw_fn)
+    if cache:
+        os.makedirs(CACHE, exist_ok=True)
+        art.save_codebook(path + ".tmp", cb)
+        os.replace(path + ".tmp", path)
+        cb = art.load_codebook(path)
+    return cb
+
+
+def prepare_campaign(cfg, cache=True, kmeans_fn=None, draw_fn=None):
+    """prepare_campaign (driver.cpp:166-187): basis + codebook artifacts."""
+    basis = load_or_build_basis(cfg, cache)
+    if cfg["m"] > basis["eigenvalues"].size:
+        raise ValueError("mode-count-out-of-range")
+    cb = load_or_build_codebook(cfg, basis, cache, kmeans_fn, draw_fn)
+    return dict(basis=basis, codebook=cb)
+
+
+def draw_realizations(cfg, n_kl, n=None, index0=0, threads=None):
+    """draw_realizations (driver.cpp:189-191): n x n_kl draws from master_seed."""
+    from . import lib
+    return lib.draw_standard_normal(cfg["n_realizations"] if n is None else n, n_kl, cfg["master_seed"], index0,
+                                    threads)
+
+
+def make_context(cfg, artifacts, device=0, factor=True):
+    from . import lib
+    ctx = lib.Context(cfg["dim"], cfg["mesh_resolution"], artifacts["basis"], artifacts["codebook"], cfg["precond"],
+                      device)
+    if factor:
+        ctx.factor_centroids()
+    return ctx
+
+
+def report_from(res, codebook):
+    """SimulationReport fields (driver.hpp:65-75) from the per-sample arrays."""
+    P = codebook["P"]
+    cen = np.asarray(codebook["centroids"])
+    per = []
+    for p in range(P):
+        cc = int(res["conv_count"][p])
+        per.append(dict(n_p=int(res["n_p"][p]), sum_j=int(res["sum_j"][p]),
+                        mean_j=(int(res["conv_sum"][p]) / cc) if cc else 0.0,
+                        centroid_norm=float(np.sqrt(np.sum(cen[p] * cen[p])))))
+    sums = [c["sum_j"] for c in per]
+    return dict(n_realizations=int(len(res["labels"])), per_centroid=per,
+                mean_j=(res["conv_sum_total"] / res["conv_total"]) if res["conv_total"] else 0.0,
+                total_iterations=res["total_iterations"], max_sum_j=max(sums) if sums else 0,
+                min_sum_j=min(sums) if sums else 0, unconverged=res["unconverged"])
+
+
+def run_campaign_with(cfg, artifacts, xi, ctx=None, chunk=None):
+    """run_campaign_with (driver.cpp:193-281) on the GPU."""
+    own = ctx is None
+    if own:
+        ctx = make_context(cfg, artifacts)
+    try:
+        res = ctx.run_campaign(xi, cfg["eps"], -1, cfg.get("chunk", 0) if chunk is None else chunk)
+    finally:
+        if own:
+            ctx.close()
+    res["report"] = report_from(res, artifacts["codebook"])
+    return res

@@ -1,0 +1,34 @@
+// common.cuh — shared device helpers for the vqpc kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "vqpc.h"
+
+#define VQPC_FULL_MASK 0xffffffffu
+
+namespace vqpc {
+
+// double shuffles (two 32-bit SHFLs each)
+__device__ __forceinline__ double shfl_down(double v, int off) {
+  return __shfl_down_sync(VQPC_FULL_MASK, v, off);
+}
+__device__ __forceinline__ double shfl_up(double v, int off) {
+  return __shfl_up_sync(VQPC_FULL_MASK, v, off);
+}
+__device__ __forceinline__ double shfl_xor(double v, int off) {
+  return __shfl_xor_sync(VQPC_FULL_MASK, v, off);
+}
+
+// Butterfly all-reduce: every lane ends with bit-identical sums (IEEE addition
+// is commutative, so partner lanes compute the same value at every level).
+__device__ __forceinline__ double warp_allsum(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += shfl_xor(v, off);
+  return v;
+}
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace vqpc

@@ -1,0 +1,122 @@
+// realise.cuh — kernel (a): KL realisation kappa = exp(W Phi), W = sqrt(Lambda) .* Xi.
+//
+// Replaces lift (proj/src/field.cpp:113-125) + transport (:138-145) for a batch
+// of samples: log kappa (B x N) = W (B x K) * Phi (K x N) with
+// W_bk = sqrt(lambda_k) * xi_bk (the reference's `w`, same IEEE product) and
+// Phi mode-major (field.hpp:25). The contraction runs on the FP64 tensor pipe
+// (DMMA, mma.sync.m8n8k4.f64 — tcgen05 has no f64 kind); the exp epilogue
+// writes kappa (the only per-element quantity the matrix-free solvers need)
+// and flags samples with a non-finite value ("coefficient-overflow").
+// Summation order differs from the reference's k-outer AXPY: kappa agrees to
+// rounding (~1e-15 relative), checked in tests.
+//
+// Tiling: CTA = 64 samples x 128 points, 8 warps as 2 (samples) x 4 (points),
+// warp tile 32 x 32 = 4 x 4 DMMA tiles (32 fp64 accumulators per lane).
+// K is staged through shared memory in blocks of 16 (zero padded).
+#pragma once
+#include "common.cuh"
+
+namespace vqpc {
+
+constexpr int RL_BM = 64, RL_BN = 128, RL_BK = 16, RL_THREADS = 256;
+constexpr int RL_WLD = RL_BK + 1;   // padded row stride of the W tile
+constexpr int RL_PLD = RL_BN + 4;   // padded row stride of the Phi tile
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+struct RealiseParams {
+  const double* xi;        // B x ld (rows), first K_use columns used
+  int64_t ld;
+  int64_t B;
+  const double* sqrt_lam;  // >= K_use
+  const double* phi;       // n_kl x n_nodes mode-major
+  int n_nodes;
+  int K_use;               // modes lifted (m)
+  double* kappa;           // B x ldk
+  int64_t ldk;
+  uint8_t* flag;           // per sample; set to 1 on a non-finite kappa (nullable)
+};
+
+static __global__ void __launch_bounds__(RL_THREADS) realise_kernel(const RealiseParams prm) {
+  __shared__ double sW[RL_BM * RL_WLD];
+  __shared__ double sP[RL_BK * RL_PLD];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps
+  const int64_t b0 = static_cast<int64_t>(blockIdx.y) * RL_BM;
+  const int i0 = blockIdx.x * RL_BN;
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+
+  for (int k0 = 0; k0 < prm.K_use; k0 += RL_BK) {
+    __syncthreads();
+    // W tile: 64 x 16, w = sqrt(lambda_k) * xi (no contraction)
+    for (int e = tid; e < RL_BM * RL_BK; e += RL_THREADS) {
+      const int rb = e / RL_BK, kk = e % RL_BK;
+      const int64_t b = b0 + rb;
+      const int k = k0 + kk;
+      double v = 0.0;
+      if (b < prm.B && k < prm.K_use) v = __dmul_rn(prm.sqrt_lam[k], prm.xi[b * prm.ld + k]);
+      sW[rb * RL_WLD + kk] = v;
+    }
+    // Phi tile: 16 x 128 (coalesced along points)
+    for (int e = tid; e < RL_BK * RL_BN; e += RL_THREADS) {
+      const int kk = e / RL_BN, ii = e % RL_BN;
+      const int k = k0 + kk, i = i0 + ii;
+      sP[kk * RL_PLD + ii] = (k < prm.K_use && i < prm.n_nodes)
+                                 ? prm.phi[static_cast<size_t>(k) * prm.n_nodes + i]
+                                 : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < RL_BK; ks += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)  // A (8x4 row): row = lane/4, col = lane%4
+        af[a] = sW[(wm * 32 + a * 8 + (lane >> 2)) * RL_WLD + ks + (lane & 3)];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)  // B (4x8 col): k = lane%4, n = lane/4
+        bf[c] = sP[(ks + (lane & 3)) * RL_PLD + wn * 32 + c * 8 + (lane >> 2)];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dmma_8x8x4(acc[a][c][0], acc[a][c][1], af[a], bf[c]);
+    }
+  }
+  // epilogue: C (8x8): row = lane/4, cols = 2*(lane%4) + {0,1}
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int64_t b = b0 + wm * 32 + a * 8 + (lane >> 2);
+    if (b >= prm.B) continue;
+    bool bad = false;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = i0 + wn * 32 + c * 8 + 2 * (lane & 3);
+      const double k0v = exp(acc[a][c][0]);
+      const double k1v = exp(acc[a][c][1]);
+      double* dst = prm.kappa + b * prm.ldk + i;
+      if (i + 1 < prm.n_nodes) {
+        bad |= !isfinite(k0v) || !isfinite(k1v);
+        if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+          *reinterpret_cast<double2*>(dst) = make_double2(k0v, k1v);
+        } else {
+          dst[0] = k0v;
+          dst[1] = k1v;
+        }
+      } else if (i < prm.n_nodes) {
+        bad |= !isfinite(k0v);
+        dst[0] = k0v;
+      }
+    }
+    if (bad && prm.flag) prm.flag[b] = 1;
+  }
+}
+
+}  // namespace vqpc

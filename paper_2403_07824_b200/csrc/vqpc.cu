@@ -1,0 +1,720 @@
+// vqpc.cu — context, device memory and the C-ABI entry points (include/vqpc.h).
+//
+// Host orchestration of the hot path, restating run_campaign_with
+// (proj/src/driver.cpp:193-281) over device kernels:
+//   assign (b) -> bucket (c) -> realise (a) -> pcg (d) -> per-centroid stats,
+// chunk by chunk, after the one-time centroid factorisation (e).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "assign.cuh"
+#include "bucket.cuh"
+#include "common.cuh"
+#include "factor.cuh"
+#include "pcg1d.cuh"
+#include "realise.cuh"
+#include "vqpc.h"
+
+using namespace vqpc;
+
+namespace {
+
+struct CudaError {
+  int code;
+  std::string msg;
+};
+
+#define CK(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      throw CudaError{e_ == cudaErrorMemoryAllocation ? VQPC_OUT_OF_MEMORY : VQPC_CUDA_ERROR,     \
+                      std::string(#call) + ": " + cudaGetErrorString(e_)};                        \
+  } while (0)
+
+struct ApiError {
+  int code;
+  std::string msg;
+};
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t count) {
+    if (count <= n) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    n = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+int check_device(int device) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count <= device || device < 0) return VQPC_NO_DEVICE;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return VQPC_NO_DEVICE;
+  if (prop.major < 10) return VQPC_NO_DEVICE;  // built for sm_100a only
+  return VQPC_OK;
+}
+
+}  // namespace
+
+struct vqpc_ctx {
+  vqpc_problem pb{};
+  int n = 0;        // unknowns per sample system
+  int NP = 0;       // padded rows per factor (R*T of the pcg variant)
+  int pcgR = 0, pcgT = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool factored = false;
+  int64_t launches = 0;
+  std::string last_error;
+  std::vector<double> h_lambdas;
+  // device-resident problem data
+  DBuf<double> phi, sqrt_lam, root, sites, kappa_c;
+  DBuf<double2> fac;
+  // work buffers
+  DBuf<double> xi, kappa, best, dvec;
+  DBuf<uint8_t> kflag, status;
+  DBuf<int32_t> labels, perm, counts, iters, mia;
+  DBuf<int64_t> offsets, stats;
+  DBuf<double> rel, x;
+  DBuf<int> counter, err;
+  // optional per-kernel CUDA-event timing (bench roofline)
+  bool prof = false;
+  struct Rec {
+    int kind;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  double prof_ms[VQPC_NKINDS] = {};
+  int64_t prof_n[VQPC_NKINDS] = {};
+};
+
+namespace {
+
+double h_of(const vqpc_problem& pb) { return 1.0 / pb.size; }
+
+void launch_check(vqpc_ctx* c) {
+  ++c->launches;
+  CK(cudaGetLastError());
+}
+
+cudaEvent_t take_event(vqpc_ctx* c) {
+  if (c->pool.empty()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+  }
+  cudaEvent_t e = c->pool.back();
+  c->pool.pop_back();
+  return e;
+}
+
+// RAII bracket: records CUDA events around a launch on the context's stream
+struct Timed {
+  vqpc_ctx* c;
+  int kind;
+  cudaEvent_t a = nullptr;
+  Timed(vqpc_ctx* c_, int kind_) : c(c_), kind(kind_) {
+    if (c->prof) {
+      a = take_event(c);
+      CK(cudaEventRecord(a, c->stream));
+    }
+  }
+  ~Timed() {
+    if (c->prof && a) {
+      cudaEvent_t b = take_event(c);
+      cudaEventRecord(b, c->stream);
+      c->recs.push_back({kind, a, b});
+    }
+  }
+};
+
+// ---- pcg variant table: rows per thread R, threads T (n <= R*T) ------------
+using PcgFn = void (*)(const Pcg1dParams);
+struct PcgVariant {
+  int R, T;
+  PcgFn fn;
+  size_t smem;
+};
+
+template <int R, int T>
+PcgVariant make_variant() {
+  return PcgVariant{R, T, &pcg1d_kernel<R, T>, pcg1d_smem_bytes<R, T>()};
+}
+
+const PcgVariant* pick_pcg(int n) {
+  static const PcgVariant table[] = {
+      make_variant<16, 64>(), make_variant<16, 128>(), make_variant<16, 256>(), make_variant<16, 512>()};
+  for (const auto& v : table)
+    if (n <= v.R * v.T) return &v;
+  return nullptr;
+}
+
+// ---- assign dispatch ---------------------------------------------------------
+using AssignFn = void (*)(const AssignParams);
+template <int M>
+AssignFn assign_fn(int split) {
+  return split == 1 ? &assign_kernel<M, 1> : split == 4 ? &assign_kernel<M, 4> : &assign_kernel<M, 8>;
+}
+AssignFn pick_assign(int m, int split) {
+  switch (m) {
+#define VQPC_M(k) \
+  case k: return assign_fn<k>(split);
+    VQPC_M(1) VQPC_M(2) VQPC_M(3) VQPC_M(4) VQPC_M(5) VQPC_M(6) VQPC_M(7) VQPC_M(8) VQPC_M(9) VQPC_M(10)
+    VQPC_M(11) VQPC_M(12) VQPC_M(13) VQPC_M(14) VQPC_M(15) VQPC_M(16) VQPC_M(32) VQPC_M(64)
+#undef VQPC_M
+    default:
+      return split == 1 ? &assign_kernel_generic<1> : split == 4 ? &assign_kernel_generic<4> : &assign_kernel_generic<8>;
+  }
+}
+
+void run_assign(vqpc_ctx* c, const double* d_xi, int64_t B, int64_t ld, const double* d_root, const double* d_sites,
+                int P, int m, int32_t* d_labels, double* d_best) {
+  if (B <= 0) return;
+  if (m > 256) throw ApiError{VQPC_INVALID_ARGUMENT, "m > 256 not supported"};
+  const int64_t target = static_cast<int64_t>(c->sm_count) * 1024;
+  int split = 1;
+  if (B * 1 < target && P >= 32) split = 8;
+  else if (B < 2 * target && P >= 16) split = 4;
+  AssignParams prm{d_xi, ld, B, d_root, d_sites, P, m, d_labels, d_best};
+  const int64_t threads = B * split;
+  const int blocks = static_cast<int>(ceil_div(threads, AS_THREADS));
+  AssignFn fn = pick_assign(m, split);
+  const size_t smem = AS_TILE_DOUBLES * sizeof(double);
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  Timed tm(c, VQPC_K_ASSIGN);
+  fn<<<blocks, AS_THREADS, smem, c->stream>>>(prm);
+  launch_check(c);
+}
+
+void run_realise(vqpc_ctx* c, const double* d_xi, int64_t B, int64_t ld, int K_use, double* d_kappa, int64_t ldk,
+                 uint8_t* d_flag) {
+  if (B <= 0) return;
+  RealiseParams prm{d_xi, ld, B, c->sqrt_lam.p, c->phi.p, c->pb.n_nodes, K_use, d_kappa, ldk, d_flag};
+  dim3 grid(static_cast<unsigned>(ceil_div(c->pb.n_nodes, RL_BN)), static_cast<unsigned>(ceil_div(B, RL_BM)));
+  Timed tm(c, VQPC_K_REALISE);
+  realise_kernel<<<grid, RL_THREADS, 0, c->stream>>>(prm);
+  launch_check(c);
+}
+
+void run_bucket(vqpc_ctx* c, const int32_t* d_labels, int64_t B, int32_t* d_perm, int64_t* d_offsets) {
+  const int P = c->pb.P;
+  if (B <= 0) {
+    CK(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t) * (P + 2), c->stream));
+    return;
+  }
+  const int ntiles = static_cast<int>(ceil_div(B, BK_TILE));
+  c->counts.ensure(static_cast<size_t>(P + 1) * ntiles);
+  const size_t sm = sizeof(int32_t) * (P + 1);
+  if (sm > 48 * 1024) {
+    CK(cudaFuncSetAttribute(bucket_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    CK(cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+  }
+  Timed tm(c, VQPC_K_BUCKET);
+  bucket_hist_kernel<<<ntiles, 256, sm, c->stream>>>(d_labels, B, P, ntiles, c->counts.p);
+  launch_check(c);
+  bucket_scan_kernel<<<1, 1024, 0, c->stream>>>(c->counts.p, static_cast<int64_t>(P + 1) * ntiles, P, ntiles,
+                                                d_offsets);
+  launch_check(c);
+  bucket_scatter_kernel<<<ntiles, 32, sm, c->stream>>>(d_labels, B, P, ntiles, c->counts.p, d_perm);
+  launch_check(c);
+}
+
+void run_pcg(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d_kflag, const int32_t* d_perm,
+             const int32_t* d_labels, int64_t B, int64_t out_base, double eps, int max_iter, const int32_t* d_mia,
+             int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x) {
+  if (B <= 0) return;
+  if (c->pb.dim != 1) throw ApiError{VQPC_INVALID_CONFIG, "2-D solve path not built in this version"};
+  const PcgVariant* v = pick_pcg(c->n);
+  c->counter.ensure(1);
+  CK(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->stream));
+  Pcg1dParams prm{};
+  prm.n = c->n;
+  prm.N = c->pb.size;
+  prm.h = h_of(c->pb);
+  prm.kappa = d_kappa;
+  prm.ldk = ldk;
+  prm.kflag = d_kflag;
+  prm.perm = d_perm;
+  prm.labels = d_labels;
+  prm.factors = c->fac.p;
+  prm.NP = c->NP;
+  prm.B = B;
+  prm.out_base = out_base;
+  prm.eps = eps;
+  prm.max_iter = max_iter;
+  prm.max_iter_arr = d_mia;
+  prm.counter = c->counter.p;
+  prm.iters = d_iters;
+  prm.rel = d_rel;
+  prm.status = d_status;
+  prm.x_out = d_x;
+  CK(cudaFuncSetAttribute(v->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(v->smem)));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v->fn, v->T, v->smem));
+  if (per_sm < 1) throw ApiError{VQPC_CUDA_ERROR, "pcg kernel does not fit on an SM"};
+  const int64_t grid = std::min<int64_t>(B, static_cast<int64_t>(per_sm) * c->sm_count);
+  Timed tm(c, VQPC_K_PCG);
+  v->fn<<<static_cast<unsigned>(grid), v->T, v->smem, c->stream>>>(prm);
+  launch_check(c);
+}
+
+__global__ void stats_kernel(const int32_t* labels, const int32_t* iters, const uint8_t* status, int64_t B, int P,
+                             unsigned long long* stats, unsigned long long* summary) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= B) return;
+  const int l = labels[i];
+  const unsigned long long J = static_cast<unsigned long long>(iters[i]);
+  const bool conv = status[i] == VQPC_S_CONVERGED;
+  atomicAdd(&summary[0], J);
+  atomicAdd(&summary[conv ? 2 : 1], 1ull);
+  if (conv) atomicAdd(&summary[3], J);
+  if (l < 0 || l >= P) return;
+  atomicAdd(&stats[l], 1ull);
+  atomicAdd(&stats[P + l], J);
+  if (conv) {
+    atomicAdd(&stats[2 * P + l], 1ull);
+    atomicAdd(&stats[3 * P + l], J);
+  }
+}
+
+template <class F>
+int guard(vqpc_ctx* c, F&& f) {
+  try {
+    if (c) CK(cudaSetDevice(c->pb.device));
+    f();
+    return VQPC_OK;
+  } catch (const CudaError& e) {
+    if (c) c->last_error = e.msg;
+    return e.code;
+  } catch (const ApiError& e) {
+    if (c) c->last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (c) c->last_error = "host allocation failed";
+    return VQPC_OUT_OF_MEMORY;
+  }
+}
+
+template <class T>
+void h2d(vqpc_ctx* c, T* dst, const T* src, size_t count) {
+  if (count) CK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+}
+template <class T>
+void d2h(vqpc_ctx* c, T* dst, const T* src, size_t count) {
+  if (count) CK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+}
+
+int64_t kappa_ld(const vqpc_ctx* c) { return (c->pb.n_nodes + 1) & ~1; }
+
+// The full campaign on device-resident arrays (run_campaign_with semantics).
+void campaign_device(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, double eps, int max_iter, int64_t chunk,
+                     int32_t* d_labels, int32_t* d_iters, double* d_rel, uint8_t* d_status, int64_t* d_stats,
+                     int64_t* d_summary) {
+  if (!(eps > 0.0) || eps >= 1.0) throw ApiError{VQPC_INVALID_TOLERANCE, "invalid-tolerance"};
+  if (ld < c->pb.n_kl) throw ApiError{VQPC_INVALID_ARGUMENT, "ld < n_kl"};
+  if (!c->factored) throw ApiError{VQPC_INVALID_CONFIG, "vqpc_factor_centroids must precede solves"};
+  const int P = c->pb.P;
+  if (chunk <= 0 || chunk > B) chunk = B;
+  const int64_t ldk = kappa_ld(c);
+  c->kappa.ensure(static_cast<size_t>(std::max<int64_t>(chunk, 1)) * ldk);
+  c->kflag.ensure(std::max<int64_t>(chunk, 1));
+  c->perm.ensure(std::max<int64_t>(chunk, 1));
+  c->offsets.ensure(P + 2);
+  const double* root = c->pb.method == VQPC_GRID || c->pb.method == VQPC_SIGN_GRID ? nullptr : c->root.p;
+  for (int64_t c0 = 0; c0 < B; c0 += chunk) {
+    const int64_t nb = std::min(chunk, B - c0);
+    const double* xi = d_xi + c0 * ld;
+    run_assign(c, xi, nb, ld, root, c->sites.p, P, c->pb.m, d_labels + c0, nullptr);
+    run_bucket(c, d_labels + c0, nb, c->perm.p, c->offsets.p);
+    CK(cudaMemsetAsync(c->kflag.p, 0, nb, c->stream));
+    run_realise(c, xi, nb, ld, c->pb.n_kl, c->kappa.p, ldk, c->kflag.p);
+    run_pcg(c, c->kappa.p, ldk, c->kflag.p, c->perm.p, d_labels + c0, nb, c0, eps, max_iter, nullptr, d_iters,
+            d_rel, d_status, nullptr);
+  }
+  CK(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 4 * P, c->stream));
+  CK(cudaMemsetAsync(d_summary, 0, sizeof(int64_t) * 4, c->stream));
+  Timed tm(c, VQPC_K_OTHER);
+  stats_kernel<<<static_cast<unsigned>(ceil_div(B, 256)), 256, 0, c->stream>>>(
+      d_labels, d_iters, d_status, B, P, reinterpret_cast<unsigned long long*>(d_stats),
+      reinterpret_cast<unsigned long long*>(d_summary));
+  launch_check(c);
+}
+
+}  // namespace
+
+// =============================================================================
+extern "C" {
+
+const char* vqpc_error_string(int code) {
+  switch (code) {
+    case VQPC_OK: return "ok";
+    case VQPC_INVALID_LATENT: return "invalid-latent";
+    case VQPC_INVALID_COEFFICIENT: return "invalid-coefficient";
+    case VQPC_COEFFICIENT_OVERFLOW: return "coefficient-overflow";
+    case VQPC_NOT_SPD: return "not-spd";
+    case VQPC_PCG_BREAKDOWN: return "pcg-breakdown";
+    case VQPC_INVALID_TOLERANCE: return "invalid-tolerance";
+    case VQPC_MODE_COUNT_OUT_OF_RANGE: return "mode-count-out-of-range";
+    case VQPC_INVALID_CODEBOOK: return "invalid-codebook";
+    case VQPC_INSUFFICIENT_SAMPLES: return "insufficient-samples";
+    case VQPC_INVALID_CONFIG: return "invalid-config";
+    case VQPC_INVALID_ARGUMENT: return "invalid-argument";
+    case VQPC_CUDA_ERROR: return "cuda-error";
+    case VQPC_NO_DEVICE: return "no-device";
+    case VQPC_OUT_OF_MEMORY: return "out-of-memory";
+    default: return "unknown";
+  }
+}
+
+const char* vqpc_last_error(const vqpc_ctx* c) { return c ? c->last_error.c_str() : ""; }
+int vqpc_unknowns(const vqpc_ctx* c) { return c ? c->n : 0; }
+int64_t vqpc_launch_count(const vqpc_ctx* c) { return c ? c->launches : 0; }
+
+int vqpc_ctx_create(const vqpc_problem* pb, vqpc_ctx** out) {
+  if (!pb || !out) return VQPC_INVALID_ARGUMENT;
+  *out = nullptr;
+  const int dev_ok = check_device(pb->device);
+  if (dev_ok != VQPC_OK) return dev_ok;
+  if (pb->dim != 1 && pb->dim != 2) return VQPC_INVALID_CONFIG;
+  if (pb->size < 2 || pb->n_kl < 1 || pb->P < 1 || pb->m < 0) return VQPC_INVALID_CONFIG;
+  const int n_nodes = pb->dim == 1 ? pb->size : (pb->size + 1) * (pb->size + 1);
+  if (pb->n_nodes != n_nodes) return VQPC_INVALID_CONFIG;
+  if (pb->m > pb->n_kl) return VQPC_MODE_COUNT_OUT_OF_RANGE;
+  const bool grid = pb->method == VQPC_GRID || pb->method == VQPC_SIGN_GRID;
+  if (grid && !pb->latent) return VQPC_INVALID_CODEBOOK;
+  if (pb->dim == 1 && pb->precond != VQPC_PC_CHOLESKY) return VQPC_INVALID_CONFIG;
+  auto* c = new vqpc_ctx();
+  c->pb = *pb;
+  c->n = pb->dim == 1 ? pb->size - 1 : (pb->size - 1) * (pb->size - 1);
+  const int rc = guard(c, [&] {
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, pb->device));
+    c->sm_count = prop.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+    if (pb->dim == 1) {
+      const PcgVariant* v = pick_pcg(c->n);
+      if (!v) throw ApiError{VQPC_INVALID_CONFIG, "1-D system larger than the largest pcg variant"};
+      c->pcgR = v->R;
+      c->pcgT = v->T;
+      c->NP = v->R * v->T;
+    }
+    const size_t K = pb->n_kl, nn = pb->n_nodes;
+    std::vector<double> sl(K);
+    for (size_t k = 0; k < K; ++k) {
+      if (!(pb->eigenvalues[k] >= 0.0)) throw ApiError{VQPC_INVALID_CONFIG, "negative eigenvalue"};
+      sl[k] = std::sqrt(pb->eigenvalues[k]);  // the reference's std::sqrt(lambda_k)
+    }
+    c->phi.ensure(K * nn);
+    c->sqrt_lam.ensure(K);
+    h2d(c, c->phi.p, pb->eigenvectors, K * nn);
+    h2d(c, c->sqrt_lam.p, sl.data(), K);
+    const size_t Pm = static_cast<size_t>(pb->P) * pb->m;
+    c->sites.ensure(std::max<size_t>(Pm, 1));
+    h2d(c, c->sites.p, grid ? pb->latent : pb->centroids, Pm);
+    c->h_lambdas.assign(pb->lambdas, pb->lambdas + pb->m);
+    std::vector<double> root(std::max(pb->m, 1));
+    for (int k = 0; k < pb->m; ++k) root[k] = std::sqrt(pb->lambdas[k]);  // T2Map::to_quant root
+    c->root.ensure(root.size());
+    h2d(c, c->root.p, root.data(), root.size());
+    if (pb->map == VQPC_CDF && !grid) throw ApiError{VQPC_INVALID_CONFIG, "ScaledCdf map: not on the GPU path"};
+    CK(cudaStreamSynchronize(c->stream));
+  });
+  if (rc != VQPC_OK) {
+    vqpc_ctx_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return VQPC_OK;
+}
+
+void vqpc_ctx_destroy(vqpc_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->pb.device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto* b : {&c->phi, &c->sqrt_lam, &c->root, &c->sites, &c->kappa_c, &c->xi, &c->kappa, &c->best, &c->dvec,
+                  &c->rel, &c->x})
+    b->release();
+  c->fac.release();
+  c->kflag.release();
+  c->status.release();
+  for (auto* b : {&c->labels, &c->perm, &c->counts, &c->iters, &c->mia}) b->release();
+  c->offsets.release();
+  c->stats.release();
+  c->counter.release();
+  c->err.release();
+  for (auto& r : c->recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : c->pool) cudaEventDestroy(e);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int vqpc_set_stream(vqpc_ctx* c, void* stream) {
+  if (!c) return VQPC_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    if (c->own_stream && c->stream) {
+      CK(cudaStreamSynchronize(c->stream));
+      CK(cudaStreamDestroy(c->stream));
+    }
+    c->own_stream = stream == nullptr;
+    if (stream)
+      c->stream = static_cast<cudaStream_t>(stream);
+    else
+      CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  });
+}
+
+int vqpc_synchronize(vqpc_ctx* c) {
+  if (!c) return VQPC_INVALID_ARGUMENT;
+  return guard(c, [&] { CK(cudaStreamSynchronize(c->stream)); });
+}
+
+// (e): centroid coefficients (realise over the first m modes of the latent
+// centroid chi_p, quantizer.cpp:465-476) then the per-centroid factor.
+int vqpc_factor_centroids(vqpc_ctx* c) {
+  if (!c) return VQPC_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    const vqpc_problem& pb = c->pb;
+    const int P = pb.P, m = pb.m;
+    // chi_p: latent sites for grids, T2(centroid) = eta / sqrt(lambda) for Scale
+    std::vector<double> chi(static_cast<size_t>(P) * std::max(m, 1), 0.0);
+    const bool grid = pb.method == VQPC_GRID || pb.method == VQPC_SIGN_GRID;
+    for (int p = 0; p < P; ++p)
+      for (int k = 0; k < m; ++k) {
+        const size_t e = static_cast<size_t>(p) * m + k;
+        chi[e] = grid ? pb.latent[e] : pb.centroids[e] / std::sqrt(pb.lambdas[k]);
+      }
+    c->xi.ensure(chi.size());
+    h2d(c, c->xi.p, chi.data(), chi.size());
+    const int64_t ldk = kappa_ld(c);
+    c->kappa_c.ensure(static_cast<size_t>(P) * ldk);
+    c->kflag.ensure(P);
+    CK(cudaMemsetAsync(c->kflag.p, 0, P, c->stream));
+    run_realise(c, c->xi.p, P, std::max(m, 1), m, c->kappa_c.p, ldk, c->kflag.p);
+    if (pb.dim != 1) throw ApiError{VQPC_INVALID_CONFIG, "2-D factorisation not built in this version"};
+    c->fac.ensure(static_cast<size_t>(P) * c->NP);
+    c->err.ensure(1);
+    CK(cudaMemsetAsync(c->err.p, 0, sizeof(int), c->stream));
+    factor1d_kernel<<<static_cast<unsigned>(ceil_div(P, 64)), 64, 0, c->stream>>>(c->kappa_c.p, ldk, P, c->n,
+                                                                                    h_of(pb), c->fac.p, c->NP,
+                                                                                    c->err.p);
+    launch_check(c);
+    int err = 0;
+    std::vector<uint8_t> flags(P);
+    d2h(c, &err, c->err.p, 1);
+    d2h(c, flags.data(), c->kflag.p, P);
+    CK(cudaStreamSynchronize(c->stream));
+    for (uint8_t f : flags)
+      if (f) throw ApiError{VQPC_COEFFICIENT_OVERFLOW, "coefficient-overflow in a centroid coefficient"};
+    if (err) throw ApiError{VQPC_NOT_SPD, "not-spd"};
+    c->factored = true;
+  });
+}
+
+int vqpc_centroid_coefficients(vqpc_ctx* c, double* kappa_out) {
+  if (!c || !kappa_out) return VQPC_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    if (!c->kappa_c.p) throw ApiError{VQPC_INVALID_CONFIG, "call vqpc_factor_centroids first"};
+    const int64_t ldk = kappa_ld(c);
+    CK(cudaMemcpy2DAsync(kappa_out, sizeof(double) * c->pb.n_nodes, c->kappa_c.p, sizeof(double) * ldk,
+                         sizeof(double) * c->pb.n_nodes, c->pb.P, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int vqpc_precond_apply(vqpc_ctx* c, int p, const double* r, double* z) {
+  if (!c || !r || !z) return VQPC_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    if (!c->factored) throw ApiError{VQPC_INVALID_CONFIG, "not factored"};
+    if (p < 0 || p >= c->pb.P) throw ApiError{VQPC_INVALID_ARGUMENT, "p out of range"};
+    c->dvec.ensure(2 * static_cast<size_t>(c->n));
+    h2d(c, c->dvec.p, r, c->n);
+    precond1d_apply_kernel<<<1, 1, 0, c->stream>>>(c->fac.p, c->NP, p, c->n, c->dvec.p, c->dvec.p + c->n);
+    launch_check(c);
+    d2h(c, z, c->dvec.p + c->n, c->n);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int vqpc_assign_d(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, int32_t* d_labels) {
+  if (!c) return VQPC_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    if (ld < c->pb.m) throw ApiError{VQPC_INVALID_ARGUMENT, "ld < m"};
+    const bool grid = c->pb.method == VQPC_GRID || c->pb.method == VQPC_SIGN_GRID;
+    run_assign(c, d_xi, B, ld, grid ? nullptr : c->root.p, c->sites.p, c->pb.P, c->pb.m, d_labels, nullptr);
+  });
+}
+
+int vqpc_assign(vqpc_ctx* c, const double* xi, int64_t B, int ld, int32_t* labels) {
+  if (!c) return VQPC_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    if (ld < c->pb.m) throw ApiError{VQPC_INVALID_ARGUMENT, "ld < m"};
+    c->xi.ensure(static_cast<size_t>(std::max<int64_t>(B, 1)) * ld);
+    c->labels.ensure(std::max<int64_t>(B, 1));
+    h2d(c, c->xi.p, xi, static_cast<size_t>(B) * ld);
+    const bool grid = c->pb.method == VQPC_GRID || c->pb.method == VQPC_SIGN_GRID;
+    run_assign(c, c->xi.p, B, ld, grid ? nullptr : c->root.p, c->sites.p, c->pb.P, c->pb.m, c->labels.p, nullptr);
+    d2h(c, labels, c->labels.p, B);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int vqpc_bucket_d(vqpc_ctx* c, const int32_t* d_labels, int64_t B, int32_t* d_perm, int64_t* d_offsets) {
+  if (!c) return VQPC_INVALID_ARGUMENT;
+  return guard(c, [&] { run_bucket(c, d_labels, B, d_perm, d_offsets); });
+}
+
+int vqpc_realise(vqpc_ctx* c, const double* xi, int64_t B, int ld, int m, double* kappa_out, uint8_t* status_out) {
+  if (!c) return VQPC_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    if (m < 0 || m > c->pb.n_kl) throw ApiError{VQPC_MODE_COUNT_OUT_OF_RANGE, "mode-count-out-of-range"};
+    if (ld < m) throw ApiError{VQPC_INVALID_ARGUMENT, "ld < m"};
+    const int64_t ldk = kappa_ld(c);
+    c->xi.ensure(static_cast<size_t>(std::max<int64_t>(B, 1)) * ld);
+    c->kappa.ensure(static_cast<size_t>(std::max<int64_t>(B, 1)) * ldk);
+    c->kflag.ensure(std::max<int64_t>(B, 1));
+    h2d(c, c->xi.p, xi, static_cast<size_t>(B) * ld);
+    CK(cudaMemsetAsync(c->kflag.p, 0, std::max<int64_t>(B, 1), c->stream));
+    run_realise(c, c->xi.p, B, ld, m, c->kappa.p, ldk, c->kflag.p);
+    CK(cudaMemcpy2DAsync(kappa_out, sizeof(double) * c->pb.n_nodes, c->kappa.p, sizeof(double) * ldk,
+                         sizeof(double) * c->pb.n_nodes, B, cudaMemcpyDeviceToHost, c->stream));
+    if (status_out) {
+      d2h(c, status_out, c->kflag.p, B);
+      CK(cudaStreamSynchronize(c->stream));
+      for (int64_t i = 0; i < B; ++i) status_out[i] = status_out[i] ? VQPC_S_COEFF_OVERFLOW : 0;
+    }
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int vqpc_solve_batch(vqpc_ctx* c, const double* xi, int64_t B, int ld, const int32_t* labels, double eps,
+                     int max_iter, const int32_t* max_iter_arr, int32_t* iters, double* final_rel, uint8_t* status,
+                     double* x_out) {
+  if (!c) return VQPC_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    if (!(eps > 0.0) || eps >= 1.0) throw ApiError{VQPC_INVALID_TOLERANCE, "invalid-tolerance"};
+    if (!c->factored) throw ApiError{VQPC_INVALID_CONFIG, "vqpc_factor_centroids must precede solves"};
+    if (ld < c->pb.n_kl) throw ApiError{VQPC_INVALID_ARGUMENT, "ld < n_kl"};
+    const int P = c->pb.P;
+    for (int64_t i = 0; i < B; ++i)
+      if (labels[i] < -1 || labels[i] >= P) throw ApiError{VQPC_INVALID_ARGUMENT, "label out of range"};
+    const int64_t Bm = std::max<int64_t>(B, 1);
+    const int64_t ldk = kappa_ld(c);
+    c->xi.ensure(static_cast<size_t>(Bm) * ld);
+    c->labels.ensure(Bm);
+    c->perm.ensure(Bm);
+    c->offsets.ensure(P + 2);
+    c->kappa.ensure(static_cast<size_t>(Bm) * ldk);
+    c->kflag.ensure(Bm);
+    c->iters.ensure(Bm);
+    c->rel.ensure(Bm);
+    c->status.ensure(Bm);
+    if (x_out) c->x.ensure(static_cast<size_t>(Bm) * c->n);
+    if (max_iter_arr) {
+      c->mia.ensure(Bm);
+      h2d(c, c->mia.p, max_iter_arr, B);
+    }
+    h2d(c, c->xi.p, xi, static_cast<size_t>(B) * ld);
+    h2d(c, c->labels.p, labels, B);
+    run_bucket(c, c->labels.p, B, c->perm.p, c->offsets.p);
+    CK(cudaMemsetAsync(c->kflag.p, 0, Bm, c->stream));
+    run_realise(c, c->xi.p, B, ld, c->pb.n_kl, c->kappa.p, ldk, c->kflag.p);
+    run_pcg(c, c->kappa.p, ldk, c->kflag.p, c->perm.p, c->labels.p, B, 0, eps, max_iter,
+            max_iter_arr ? c->mia.p : nullptr, c->iters.p, c->rel.p, c->status.p, x_out ? c->x.p : nullptr);
+    d2h(c, iters, c->iters.p, B);
+    d2h(c, final_rel, c->rel.p, B);
+    d2h(c, status, c->status.p, B);
+    if (x_out) d2h(c, x_out, c->x.p, static_cast<size_t>(B) * c->n);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int vqpc_profile(vqpc_ctx* c, int enable) {
+  if (!c) return VQPC_INVALID_ARGUMENT;
+  c->prof = enable != 0;
+  return VQPC_OK;
+}
+
+int vqpc_profile_read(vqpc_ctx* c, double* ms, int64_t* counts, int reset) {
+  if (!c) return VQPC_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    CK(cudaStreamSynchronize(c->stream));
+    for (auto& r : c->recs) {
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, r.a, r.b));
+      c->prof_ms[r.kind] += t;
+      c->prof_n[r.kind] += 1;
+      c->pool.push_back(r.a);
+      c->pool.push_back(r.b);
+    }
+    c->recs.clear();
+    for (int k = 0; k < VQPC_NKINDS; ++k) {
+      if (ms) ms[k] = c->prof_ms[k];
+      if (counts) counts[k] = c->prof_n[k];
+      if (reset) {
+        c->prof_ms[k] = 0.0;
+        c->prof_n[k] = 0;
+      }
+    }
+  });
+}
+
+int vqpc_run_campaign_d(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, double eps, int max_iter, int64_t chunk,
+                        int32_t* d_labels, int32_t* d_iters, double* d_rel, uint8_t* d_status, int64_t* d_stats,
+                        int64_t* d_summary) {
+  if (!c) return VQPC_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    campaign_device(c, d_xi, B, ld, eps, max_iter, chunk, d_labels, d_iters, d_rel, d_status, d_stats, d_summary);
+  });
+}
+
+int vqpc_run_campaign(vqpc_ctx* c, const double* xi, int64_t B, int ld, double eps, int max_iter, int64_t chunk,
+                      int32_t* labels, int32_t* iters, double* final_rel, uint8_t* status, int64_t* stats,
+                      int64_t* summary) {
+  if (!c) return VQPC_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    const int P = c->pb.P;
+    const int64_t Bm = std::max<int64_t>(B, 1);
+    c->xi.ensure(static_cast<size_t>(Bm) * ld);
+    c->labels.ensure(Bm);
+    c->iters.ensure(Bm);
+    c->rel.ensure(Bm);
+    c->status.ensure(Bm);
+    c->stats.ensure(4 * static_cast<size_t>(P) + 4);
+    h2d(c, c->xi.p, xi, static_cast<size_t>(B) * ld);
+    campaign_device(c, c->xi.p, B, ld, eps, max_iter, chunk, c->labels.p, c->iters.p, c->rel.p, c->status.p,
+                    c->stats.p, c->stats.p + 4 * P);
+    d2h(c, labels, c->labels.p, B);
+    d2h(c, iters, c->iters.p, B);
+    d2h(c, final_rel, c->rel.p, B);
+    d2h(c, status, c->status.p, B);
+    d2h(c, stats, c->stats.p, 4 * static_cast<size_t>(P));
+    d2h(c, summary, c->stats.p + 4 * P, 4);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,191 @@
+"""GPU parity against the CPU oracle through the C ABI."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2403_07824_b200 import campaign, lib
+from tests.helpers import compare_runs, oracle_codebook, setup_case
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name,n_real,ns", [("C1", 512, None), ("C2", 256, None)])
+def test_kmeans_bit_identical(name, n_real, ns):
+    cfg, basis, cb, _ = setup_case(name, n_real, ns)
+    q = cfg["quantizer"]
+    m = cfg["m"]
+    pilot = lib.draw_standard_normal(q["ns"], m, q["seed"])
+    assert np.array_equal(pilot, oracle.draw_standard_normal(q["ns"], m, q["seed"]))
+    lam = basis["eigenvalues"][:m]
+    c_gpu, h_gpu = lib.kmeans(pilot, lam, q["P"])
+    c_cpu, h_cpu = oracle.kmeans(pilot, lam, q["P"])
+    assert np.array_equal(c_gpu, c_cpu)
+    assert np.array_equal(h_gpu, h_cpu)
+
+
+@pytest.mark.parametrize("name,n_real", [("C1", 4096), ("C2", 8192), ("C3", 8192)])
+def test_assign_bit_exact(name, n_real):
+    cfg, basis, cb, xi = setup_case(name, n_real)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb), factor=False)
+    lab_gpu = ctx.assign(xi)
+    lab_cpu = oracle.assign(oracle_codebook(cb), xi)
+    assert np.array_equal(lab_gpu, lab_cpu)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_realise_matches_lift_transport(name):
+    cfg, basis, cb, xi = setup_case(name, 300)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb), factor=False)
+    k_gpu, st = ctx.realise(xi)
+    k_cpu, st_cpu = oracle.realise(basis["eigenvalues"], basis["eigenvectors"], xi)
+    assert not st.any() and not st_cpu.any()
+    rel = np.abs(k_gpu - k_cpu) / k_cpu
+    assert rel.max() < 1e-13, rel.max()
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_centroid_factor_apply(name):
+    cfg, basis, cb, xi = setup_case(name, 64)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    kc_gpu = ctx.centroid_coefficients()
+    kc_cpu = oracle.centroid_coefficients(oracle_codebook(cb), basis["eigenvalues"], basis["eigenvectors"])
+    assert (np.abs(kc_gpu - kc_cpu) / kc_cpu).max() < 1e-13
+    pset = oracle.PreconditionerSet.build(1, cfg["mesh_resolution"], "cholesky", oracle_codebook(cb),
+                                          basis["eigenvalues"], basis["eigenvectors"])
+    rng = np.random.default_rng(0)
+    for p in [0, cb["P"] // 2, cb["P"] - 1]:
+        r = rng.standard_normal(ctx.n)
+        z_gpu = ctx.precond_apply(p, r)
+        z_cpu = pset.apply(p, r)
+        # both are backward-stable solves with the centroid matrix A_p: the
+        # normwise backward error is at rounding level; the forward difference
+        # is bounded by cond(A_p) * u (cond ~ 1e7 at n = 4095)
+        rp, col, val, _ = oracle.assemble(1, cfg["mesh_resolution"], kc_cpu[p])
+        Az = lambda z: np.add.reduceat(val * z[col], rp[:-1])
+        anorm = np.abs(val).max() * 3
+        for z in (z_gpu, z_cpu):
+            assert np.linalg.norm(Az(z) - r) / (anorm * np.linalg.norm(z)) < 1e-14
+        assert np.linalg.norm(z_gpu - z_cpu) / np.linalg.norm(z_cpu) < 1e-9
+
+
+def _borderline(pset, cfg, basis, xi, labels, idx, j_a, j_b, factor=4.0):
+    """True when the oracle's true-residual trace stays within [eps/f, f*eps]
+    over the iterations where the two runs disagree (rtol 1e-8
+    sits at the attainable accuracy, so a rounding-level change moves the
+    first crossing)."""
+    eps = cfg["eps"]
+    kappa, _ = oracle.realise(basis["eigenvalues"], basis["eigenvectors"], xi[idx:idx + 1])
+    tr = pset.pcg(int(labels[idx]), kappa[0], eps, trace=True)["trace"]
+    lo, hi = min(j_a, j_b), max(j_a, j_b)
+    seg = tr[lo - 1:hi]
+    return bool(seg.size and seg.max() <= factor * eps and seg.min() >= eps / factor), seg
+
+
+def _campaign_parity(name, n_real):
+    cfg, basis, cb, xi = setup_case(name, n_real)
+    ocb = oracle_codebook(cb)
+    res = campaign.run_campaign_with(cfg, dict(basis=basis, codebook=cb), xi)
+    args = (1, cfg["mesh_resolution"], "cholesky", ocb, basis["eigenvalues"], basis["eigenvectors"], xi, cfg["eps"])
+    ref = oracle.run_campaign(*args)
+    with oracle.fma_variant():
+        ref_fma = oracle.run_campaign(*args)
+    assert np.array_equal(res["labels"], ref["labels"])  # Appendix B.2: bit-exact
+    cmp = compare_runs(ref["iterations"], ref["status"], res["iterations"], res["status"])
+    yard = compare_runs(ref["iterations"], ref["status"], ref_fma["iterations"], ref_fma["status"])
+    return cfg, basis, cb, xi, res, ref, cmp, yard
+
+
+def _check_j_parity(name, n_real):
+    """Appendix B.3/B.4 against a yardstick: the same oracle built with FMA
+    contraction (a rounding-level change of the reference itself)."""
+    cfg, basis, cb, xi, res, ref, cmp, yard = _campaign_parity(name, n_real)
+    print(name, "gpu:", {k: v for k, v in cmp.items() if k != "disagree"}, "fma-yardstick:",
+          {k: v for k, v in yard.items() if k != "disagree"})
+    assert cmp["status_agree"] >= min(yard["status_agree"], 0.995) - 0.01, (cmp, yard)
+    assert cmp["frac_dj"] <= max(2 * yard["frac_dj"], 0.01), (cmp, yard)
+    # mean J over converged-both samples: within the yardstick's own spread
+    # (the reference and its FMA build already differ in the 2nd decimal on C2)
+    assert abs(cmp["mean_cpu"] - cmp["mean_gpu"]) <= max(3 * abs(yard["mean_cpu"] - yard["mean_gpu"]), 0.03), cmp
+    # every sample with |dJ| > 1 must be a borderline (flat-residual) case
+    pset = oracle.PreconditionerSet.build(1, cfg["mesh_resolution"], "cholesky", oracle_codebook(cb),
+                                          basis["eigenvalues"], basis["eigenvectors"])
+    jc, jg = ref["iterations"], res["iterations"]
+    both = (ref["status"] == 0) & (res["status"] == 0)
+    big = np.nonzero(both & (np.abs(jc.astype(np.int64) - jg) > 1))[0]
+    for i in big[:50]:
+        ok, seg = _borderline(pset, cfg, basis, xi, ref["labels"], i, int(jc[i]), int(jg[i]))
+        assert ok, (i, jc[i], jg[i], seg)
+    return cmp
+
+
+def test_campaign_C1_full():
+    cmp = _check_j_parity("C1", 4096)
+    assert cmp["n_both"] > 4000
+
+
+@pytest.mark.parametrize("name,n_real", [("C2", 1024), ("C3", 1024)])
+def test_campaign_subsets(name, n_real):
+    _check_j_parity(name, n_real)
+
+
+def _fixed_k_x(pset, basis, xi, labels, K, want_x=True):
+    _, _, _, x = pset.solve_batch(basis["eigenvalues"], basis["eigenvectors"], xi, labels, 1e-300, max_iter_arr=K,
+                                  want_x=want_x)
+    return x
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_fixed_K_solutions(name):
+    """Appendix B.5: both sides run exactly K = min(J_cpu, J_gpu) iterations
+    (eps = 1e-300, max_iter = K) and x must agree to 1e-10 in relative l2.
+    Yardstick: the same comparison between the oracle and its FMA-contracted
+    build; the GPU must be at least as close as that rounding-level variant of
+    the reference wherever 1e-10 is not met."""
+    cfg, basis, cb, xi = setup_case(name, 96)
+    ocb = oracle_codebook(cb)
+    labels = oracle.assign(ocb, xi)
+    L, V = basis["eigenvalues"], basis["eigenvectors"]
+    pset = oracle.PreconditionerSet.build(1, cfg["mesh_resolution"], "cholesky", ocb, L, V)
+    j_cpu, _, s_cpu, _ = pset.solve_batch(L, V, xi, labels, cfg["eps"])
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    j_gpu, _, s_gpu, _ = ctx.solve_batch(xi, labels, cfg["eps"])
+    both = (s_cpu == 0) & (s_gpu == 0)
+    K = np.minimum(j_cpu, j_gpu).astype(np.int32)
+    K[~both] = np.minimum(K[~both], 20)
+    x_cpu = _fixed_k_x(pset, basis, xi, labels, K)
+    jg, _, _, x_gpu = ctx.solve_batch(xi, labels, 1e-300, max_iter_arr=K, want_x=True)
+    assert np.array_equal(jg, K)
+    err = np.linalg.norm(x_gpu - x_cpu, axis=1) / np.linalg.norm(x_cpu, axis=1)
+    with oracle.fma_variant():
+        pf = oracle.PreconditionerSet.build(1, cfg["mesh_resolution"], "cholesky", ocb, L, V)
+        x_fma = _fixed_k_x(pf, basis, xi, labels, K)
+    yard = np.linalg.norm(x_fma - x_cpu, axis=1) / np.linalg.norm(x_cpu, axis=1)
+    print(name, "x rel-l2: gpu median %.2e p90 %.2e max %.2e | fma-yardstick median %.2e p90 %.2e max %.2e" % (
+        np.median(err), np.quantile(err, 0.9), err.max(), np.median(yard), np.quantile(yard, 0.9), yard.max()))
+    assert np.median(err) <= 1e-10
+    for q in (0.5, 0.9, 1.0):
+        assert np.quantile(err, q) <= max(1e-10, 3 * np.quantile(yard, q)), q
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_exact_factor_gives_one_iteration(name):
+    """xi equal to a centroid's latent point gives J = 1."""
+    cfg, basis, cb, _ = setup_case(name, 16)
+    K = basis["eigenvalues"].size
+    m = cfg["m"]
+    chi = cb["centroids"] / np.sqrt(cb["lambdas"])[None, :]
+    xi = np.zeros((cb["P"], K))
+    xi[:, :m] = chi
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    labels = np.arange(cb["P"], dtype=np.int32)
+    it, rel, st, _ = ctx.solve_batch(xi, labels, cfg["eps"])
+    assert (st == 0).all() and (it == 1).all(), (it, st)
+
+
+def test_determinism_across_chunks():
+    cfg, basis, cb, xi = setup_case("C1", 2048)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    a = ctx.run_campaign(xi, cfg["eps"], chunk=0)
+    b = ctx.run_campaign(xi, cfg["eps"], chunk=300)
+    for k in ("labels", "iterations", "rel", "status", "n_p", "sum_j"):
+        assert np.array_equal(a[k], b[k]), k
