@@ -115,6 +115,22 @@ def ref():
         R.vqpref_mesh_fingerprint.restype = U64
         R.vqpref_mesh_fingerprint.argtypes = [I]
         R.vqpref_last_error.restype = C.c_char_p
+        CP = C.c_char_p
+        sigs = {
+            "vqpref_assemble_2d": [I, VP, VP, VP, VP, VP, VP, VP],
+            "vqpref_lumped_mass": [I, VP],
+            "vqpref_assign": [I, I, I, I, VP, VP, VP, I64, I, VP],
+            "vqpref_kmeans": [VP, I, I, VP, I, I, U64, I, D, VP, VP, VP],
+            "vqpref_grid_latent_sites": [I, D, VP],
+            "vqpref_centroid_coefficient": [I, I, I, I, VP, VP, I, VP, VP, I, I, VP],
+            "vqpref_load_codebook": [CP, VP, VP, VP, VP, VP, VP],
+            "vqpref_save_codebook": [CP, I, I, I, I, VP, VP, U64],
+            "vqpref_load_kl_basis": [CP, VP, VP, VP, VP, VP, VP],
+            "vqpref_save_kl_basis": [CP, I, I, VP, VP, VP, D, D, D, I, U64],
+        }
+        for name, args in sigs.items():
+            getattr(R, name).restype = I
+            getattr(R, name).argtypes = args
         _ref = R
     return _ref
 
