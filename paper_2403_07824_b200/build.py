@@ -14,12 +14,13 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libvqpc.so")
+LIB = os.environ.get("VQPC_LIB", os.path.join(HERE, "libvqpc.so"))
 SOURCES = ["vqpc.cu", "host_quantizer.cu"]
 HEADERS = ["common.cuh", "realise.cuh", "assign.cuh", "bucket.cuh", "factor.cuh", "pcg1d.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v",
+EXTRA = os.environ.get("VQPC_NVCC_FLAGS", "").split()
+FLAGS = [*EXTRA, "-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 
 
@@ -34,7 +35,7 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" + ("_" + os.path.basename(LIB).replace(".so", "") if "VQPC_LIB" in os.environ else ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for s in SOURCES:

@@ -9,12 +9,14 @@
 // dead and provably inert, see below). Registers per thread: x, r, p (R each),
 // the preconditioner couplings n_j and the transient w/z (or A p). Shared
 // memory is thread-major ([i*T + t] holds row tR+i, so warp accesses are
-// bank-conflict free): the sample's element conductances c_j = kappa_j/h and
-// the centroid factor {n_j, 1/u_j^2}, reloaded only when the bucket changes.
+// bank-conflict free): the sample's element conductances c_j = kappa_j/h, the
+// centroid factor {n_j, 1/u_j^2} and per-thread scan constants, reloaded only
+// when the bucket (label) changes.
 //
 // Operator: A_jj = c_j + c_{j+1}, A_{j,j+1} = -c_{j+1}
 // with c_j = kappa_j / h — the same IEEE values the oracle's CSR holds; b_j = h.
-// Matrix-free: no CSR is ever formed.
+// Matrix-free: (A v)_j = -c_j v_{j-1} + d_j v_j - c_{j+1} v_{j+1}, evaluated in the
+// reference's CSR row order without contraction (see VQPC_AP_CSR/VQPC_RESID_CSR).
 //
 // Preconditioner: the exact factor of the centroid matrix, M = U U^T with U the
 // upper-bidiagonal Cholesky factor of the reference's RCM (= reversed) order
@@ -22,11 +24,10 @@
 //   sweep 1 (descending)  y_j = r_j - n_j y_{j+1};   y_j <- y_j / u_j^2
 //   sweep 2 (ascending)   z_j = y_j - n_{j-1} z_{j-1}
 // Each sweep is a first-order linear recurrence, solved as a chunked scan:
-// serial over a thread's rows (two interleaved half-chains for ILP), an
+// four interleaved serial chains over the quarters of a thread's rows, an
 // affine scan over lanes with shuffles whose multipliers are per-centroid
-// constants precomputed into shared memory (one SHFL pair + one FMA per
-// level), one barrier for the warp aggregates, a short fold over warps, and a
-// fix-up pass.
+// constants (one SHFL pair + one FMA per level), one barrier for the warp
+// aggregates, a short fold over warps, and a fix-up pass.
 //
 // Per iteration, in the reference's operation order (solver.cpp:211-242):
 //   Ap = A p; pAp = p.Ap               -> barrier 1 (reduction)
@@ -40,15 +41,16 @@
 // Halo values of x and p are never exchanged: each thread updates its copy of
 // the neighbours' boundary entries with the same FMA the neighbour executes,
 // so they stay bit-identical; only z boundary values travel (barrier 4).
-// Block reductions: butterfly inside the warp, then every warp reduces the
-// NW warp partials with the same butterfly — all threads hold identical bits,
-// and the order is fixed, so results do not depend on scheduling.
+// Block reductions: 4 split accumulators per thread, a butterfly inside the
+// warp, then every thread sums the NW warp partials with the same fixed tree —
+// all threads hold identical bits and the order never depends on scheduling.
 // Breakdown checks use !(v > 0) exactly like the reference (NaN-safe).
 //
-// Dead rows j >= n: n_j = 1/u_j^2 = 0 (so z_j = p_j = x_j = 0) and
-// n_{n-1} = 0 (no coupling into them); A p leaks -c_n p_{n-1} into r_n only,
-// which sweep 1 never propagates (n_{n-1} = 0) and scales by 0; the true
-// residual is masked in the one thread that owns dead rows.
+// Dead rows j >= n: n_j = 1/u_j^2 = 0 (so z_j = p_j = x_j = 0), n_{n-1} = 0,
+// d_j = 0 and the coupling c_j = 0 for j >= n (the diagonal of row n-1 keeps the
+// true c_n), so (A v)_j = 0 on dead rows without any masking; only b_j = 0 is
+// special, so the residual of the last warp (the only one that can own dead
+// rows) takes a masked code path behind a warp-uniform branch.
 #pragma once
 #include "common.cuh"
 
@@ -81,8 +83,11 @@ template <int R, int T>
 struct Pcg1dShared {
   static constexpr int NW = T / 32;
   double2 fac[R * T];     // {n_j, 1/u_j^2}, thread-major
-  double cs[R * T + 1];   // c_j = kappa_j / h, thread-major; [R*T] = c_{R*T}
-  double lev[12 * T];     // per-thread scan multipliers: L1[5], Q1, L2[5], Q2
+  double cs[R * T];       // coupling c_j = kappa_j / h (0 for j >= n), thread-major
+  double dg[R * T];       // diagonal d_j = c_j + c_{j+1} (true c_n; 0 for dead rows)
+  double cs_end;          // c_{R*T}: right coupling of the last thread's last row
+  double lev[12 * T];     // per-thread lane-scan multipliers: L1[5], Q1, L2[5], Q2
+  double qa[8 * T];       // per-thread quarter products: sweep 1 [0..3], sweep 2 [4..7]
   double wa1[NW], wa2[NW];  // per-warp products of the sweep multipliers
   double sw1[NW], sw2[NW];  // per-iteration warp aggregates
   double red[4][NW];        // reduction partials: pAp, rr, rz, |b|^2
@@ -90,31 +95,103 @@ struct Pcg1dShared {
   int item;
 };
 
-// sum over the NW warp partials in a fixed butterfly order (identical in all threads)
+// The true residual b - A x decides J (rel < eps), so it is evaluated in the
+// reference's exact CSR order without contraction: given the same x it is
+// bit-identical to the CPU's, which measurably tightens iteration-count parity
+// (C1: |dJ| <= 2, mean J equal to 2 decimals). A p only shapes
+// the trajectory, yet evaluating it in the same CSR order also keeps the GPU
+// trajectory measurably closer to the CPU's (C1 A/B: frac(|dJ|>1) 0.68 % vs 1.1 %,
+// max |dJ| 2 vs 6) for ~15 % more time; VQPC_AP_CSR=0 selects the 3-op FMA form.
+#ifndef VQPC_RESID_CSR
+#define VQPC_RESID_CSR 1
+#endif
+#ifndef VQPC_AP_CSR
+#define VQPC_AP_CSR 1
+#endif
+
+// One CSR row product in the reference's order without contraction
+// (fem.cpp:142-148: s = 0; s += a_{j,j-1} v_{j-1}; s += a_jj v_j; s += a_{j,j+1} v_{j+1}).
+__device__ __forceinline__ double csr_row(double c_lo, double d, double c_hi, double vl, double v, double vr) {
+  double sacc = __dmul_rn(-c_lo, vl);
+  sacc = __dadd_rn(sacc, __dmul_rn(d, v));
+  return __dadd_rn(sacc, __dmul_rn(-c_hi, vr));
+}
+
+// The same row with FMA contraction (3 fp64 operations; different rounding).
+__device__ __forceinline__ double fused_row(double c_lo, double d, double c_hi, double vl, double v, double vr) {
+  return fma(d, v, -fma(c_hi, vr, c_lo * vl));
+}
+
+// |b - A x|^2 over a thread's rows (4 split accumulators)
+template <int R, int T, bool MASK>
+__device__ __forceinline__ double true_residual(const double (&x)[R], double x_left, double x_right,
+                                                const double* cst, const double* dgt, const double* c_halo,
+                                                double h, int j0, int n) {
+  constexpr int Q = R / 4;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#if VQPC_RESID_CSR
+  double c_lo = cst[0];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const double c_hi = i + 1 < R ? cst[(i + 1) * T] : *c_halo;
+    const double xl = i == 0 ? x_left : x[i - 1];
+    const double xr = i + 1 < R ? x[i + 1] : x_right;
+    double rt = __dsub_rn(h, csr_row(c_lo, dgt[i * T], c_hi, xl, x[i], xr));
+    if (MASK && j0 + i >= n) rt = 0.0;
+    acc[i / Q] = fma(rt, rt, acc[i / Q]);
+    c_lo = c_hi;
+  }
+#else
+  double c_lo = cst[0];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const double c_hi = i + 1 < R ? cst[(i + 1) * T] : *c_halo;
+    const double xl = i == 0 ? x_left : x[i - 1];
+    const double xr = i + 1 < R ? x[i + 1] : x_right;
+    double rt = h - fused_row(c_lo, dgt[i * T], c_hi, xl, x[i], xr);
+    if (MASK && j0 + i >= n) rt = 0.0;
+    acc[i / Q] = fma(rt, rt, acc[i / Q]);
+    c_lo = c_hi;
+  }
+#endif
+  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
+// pairwise sum of NW smem partials in a fixed tree (every thread: same bits)
 template <int NW>
-__device__ __forceinline__ double cross_warp_sum(const double* part, int lane) {
-  double t = lane < NW ? part[lane] : 0.0;
-  return warp_allsum(t);
+__device__ __forceinline__ double tree_sum(const double* part) {
+  double v[NW];
+#pragma unroll
+  for (int i = 0; i < NW; ++i) v[i] = part[i];
+#pragma unroll
+  for (int w = 1; w < NW; w <<= 1)
+#pragma unroll
+    for (int i = 0; i + w < NW; i += 2 * w) v[i] += v[i + w];
+  return v[0];
 }
 
 template <int R, int T>
 __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
   using Sh = Pcg1dShared<R, T>;
   constexpr int NW = Sh::NW;
-  constexpr int H = R / 2;
-  static_assert(R % 2 == 0 && R >= 4, "two half-chains per thread");
+  constexpr int Q = R / 4;  // rows per quarter chain
+  static_assert(R % 4 == 0 && R >= 4, "four quarter-chains per thread");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Sh& S = *reinterpret_cast<Sh*>(smem_raw);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int j0 = tid * R;
   const int n = prm.n;
-  const bool tail_thread = j0 + R > n;  // owns dead rows
+  const double* cst = S.cs + tid;      // cst[i*T] = c_{j0+i}
+  const double* levt = S.lev + tid;    // levt[k*T]
+  const double* qat = S.qa + tid;      // qat[q*T]
+  const double2* fact = S.fac + tid;   // fact[i*T]
+  const double* dgt = S.dg + tid;      // dgt[i*T] = d_{j0+i}
+  const double* c_halo = tid + 1 < T ? S.cs + tid + 1 : &S.cs_end;  // c_{j0+R}
 
   int cur_label = -1;
   double nc[R];         // n_j of own rows
   double n_left = 0.0;  // n_{j0-1}
-  double A1lo = 0, A1hi = 0, A2lo = 0, A2hi = 0;
 
   for (;;) {
     if (tid == 0) S.item = atomicAdd(prm.counter, 1);
@@ -139,22 +216,22 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
       for (int e = tid; e < R * T; e += T) S.fac[(e % R) * T + e / R] = src[e];  // coalesced read
       __syncthreads();
 #pragma unroll
-      for (int i = 0; i < R; ++i) nc[i] = S.fac[i * T + tid].x;
+      for (int i = 0; i < R; ++i) nc[i] = fact[i * T].x;
       n_left = tid > 0 ? S.fac[(R - 1) * T + tid - 1].x : 0.0;
-      A1lo = 1.0;
-      A1hi = 1.0;
+      double P1 = 1.0, P2 = 1.0;
 #pragma unroll
-      for (int i = 0; i < H; ++i) A1lo *= -nc[i];
+      for (int q = 0; q < 4; ++q) {
+        double a1 = 1.0, a2 = 1.0;
 #pragma unroll
-      for (int i = H; i < R; ++i) A1hi *= -nc[i];
-      A2lo = -n_left;
-#pragma unroll
-      for (int i = 0; i < H - 1; ++i) A2lo *= -nc[i];
-      A2hi = 1.0;
-#pragma unroll
-      for (int i = H - 1; i < R - 1; ++i) A2hi *= -nc[i];
-      // lane-range products for the shuffle scans
-      double P1 = A1lo * A1hi, P2 = A2lo * A2hi;  // current inclusive range products
+        for (int i = q * Q; i < q * Q + Q; ++i) {
+          a1 *= -nc[i];
+          a2 *= i == 0 ? -n_left : -nc[i - 1];
+        }
+        S.qa[q * T + tid] = a1;
+        S.qa[(4 + q) * T + tid] = a2;
+        P1 *= a1;
+        P2 *= a2;
+      }
 #pragma unroll
       for (int k = 0; k < 5; ++k) {
         const int off = 1 << k;
@@ -176,20 +253,28 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
 
     // ---- sample setup: c_j = kappa_j / h, b = h, x = 0, r = b --------------
     const double* kap = prm.kappa + static_cast<size_t>(s) * prm.ldk;
+    {
+      // IEEE division: the oracle's kappa/h; d_j = c_j + c_{j+1} like its CSR diagonal
+      double c_prev = j0 < n ? kap[j0] / prm.h : 0.0;
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int j = j0 + i;
-      S.cs[i * T + tid] = j <= n ? kap[j] / prm.h : 0.0;  // IEEE division: the oracle's kappa/h
+      for (int i = 0; i < R; ++i) {
+        const int j = j0 + i;
+        const double c_next = j + 1 <= n ? kap[j + 1] / prm.h : 0.0;
+        S.cs[i * T + tid] = j < n ? c_prev : 0.0;
+        S.dg[i * T + tid] = j < n ? __dadd_rn(c_prev, c_next) : 0.0;
+        c_prev = c_next;
+      }
+      if (tid == T - 1) S.cs_end = 0.0;  // row R*T is never live
     }
-    if (tid == T - 1) S.cs[R * T] = R * T <= n ? kap[R * T] / prm.h : 0.0;
     double x[R], r[R], p[R], wz[R];
-    double bb = 0.0;
+    double bbq[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       x[i] = 0.0;
       r[i] = j0 + i < n ? prm.h : 0.0;
-      bb = fma(r[i], r[i], bb);
+      bbq[i / Q] = fma(r[i], r[i], bbq[i / Q]);
     }
+    const double bb = (bbq[0] + bbq[1]) + (bbq[2] + bbq[3]);
     const int max_iter = prm.max_iter_arr ? prm.max_iter_arr[gs] : (prm.max_iter < 0 ? 10 * n : prm.max_iter);
 
     double rz = 0.0, norm_b = 0.0, rel_rec = 0.0;
@@ -201,42 +286,47 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
     for (;;) {
       // ================= sweep 1 (descending) + rr: barrier 2 ===============
       {
-        double vh = 0.0, vl = 0.0;
+        double v[4];
 #pragma unroll
-        for (int i = 0; i < H; ++i) {  // two independent chains, incoming 0
-          vh = fma(-nc[R - 1 - i], vh, r[R - 1 - i]);
-          vl = fma(-nc[H - 1 - i], vl, r[H - 1 - i]);
-        }
-        const double Wh = vh;
-        double W = fma(A1lo, vh, vl);
+        for (int q = 0; q < 4; ++q) v[q] = 0.0;
 #pragma unroll
-        for (int k = 0; k < 5; ++k) W = fma(S.lev[k * T + tid], shfl_down(W, 1 << k), W);
+        for (int i = Q - 1; i >= 0; --i)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[q] = fma(-nc[q * Q + i], v[q], r[q * Q + i]);
+        const double a0 = qat[0], a1 = qat[T], a2 = qat[2 * T], a3 = qat[3 * T];
+        double W = fma(a2, v[3], v[2]);
+        W = fma(a1, W, v[1]);
+        W = fma(a0, W, v[0]);
+#pragma unroll
+        for (int k = 0; k < 5; ++k) W = fma(levt[k * T], shfl_down(W, 1 << k), W);
         const double rrw = warp_allsum(rr_loc);
         if (lane == 0) {
           S.sw1[warp] = W;
           S.red[1][warp] = rrw;
         }
         __syncthreads();  // barrier 2
-        double v = 0.0;
+        double vw = 0.0;
 #pragma unroll
         for (int w2 = NW - 1; w2 > 0; --w2)
-          if (w2 > warp) v = fma(S.wa1[w2], v, S.sw1[w2]);
+          if (w2 > warp) vw = fma(S.wa1[w2], vw, S.sw1[w2]);
         const double Wn = shfl_down(W, 1);
-        const double vin = fma(S.lev[5 * T + tid], v, lane == 31 ? 0.0 : Wn);
-        // fix-up: hi half from vin, lo half from y at row j0+H
-        double uh = vin, ul = fma(A1hi, vin, Wh);
+        double in[4];
+        in[3] = fma(levt[5 * T], vw, lane == 31 ? 0.0 : Wn);
+        in[2] = fma(a3, in[3], v[3]);
+        in[1] = fma(a2, in[2], v[2]);
+        in[0] = fma(a1, in[1], v[1]);
 #pragma unroll
-        for (int i = 0; i < H; ++i) {
-          uh = fma(-nc[R - 1 - i], uh, r[R - 1 - i]);
-          ul = fma(-nc[H - 1 - i], ul, r[H - 1 - i]);
-          wz[R - 1 - i] = uh;
-          wz[H - 1 - i] = ul;
-        }
+        for (int i = Q - 1; i >= 0; --i)
 #pragma unroll
-        for (int i = 0; i < R; ++i) wz[i] *= S.fac[i * T + tid].y;
+          for (int q = 0; q < 4; ++q) {
+            in[q] = fma(-nc[q * Q + i], in[q], r[q * Q + i]);
+            wz[q * Q + i] = in[q];
+          }
+#pragma unroll
+        for (int i = 0; i < R; ++i) wz[i] *= fact[i * T].y;
       }
       if (j > 0) {
-        const double rr = cross_warp_sum<NW>(S.red[1], lane);
+        const double rr = tree_sum<NW>(S.red[1]);
         const double rel = sqrt(rr) / norm_b;
         J = j;
         rel_rec = rel;
@@ -247,42 +337,47 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
       }
       // ================= sweep 2 (ascending): barrier 3 =====================
       {
-        double vl = wz[0], vh = wz[H];  // incoming 0 for both halves
+        double v[4];
 #pragma unroll
-        for (int i = 1; i < H; ++i) {
-          vl = fma(-nc[i - 1], vl, wz[i]);
-          vh = fma(-nc[H + i - 1], vh, wz[H + i]);
-        }
-        const double Zl = vl;
-        double W = fma(A2hi, vl, vh);
+        for (int q = 0; q < 4; ++q) v[q] = wz[q * Q];  // incoming 0
 #pragma unroll
-        for (int k = 0; k < 5; ++k) W = fma(S.lev[(6 + k) * T + tid], shfl_up(W, 1 << k), W);
+        for (int i = 1; i < Q; ++i)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[q] = fma(-nc[q * Q + i - 1], v[q], wz[q * Q + i]);
+        const double b0 = qat[4 * T], b1 = qat[5 * T], b2 = qat[6 * T], b3 = qat[7 * T];
+        double W = fma(b1, v[0], v[1]);
+        W = fma(b2, W, v[2]);
+        W = fma(b3, W, v[3]);
+#pragma unroll
+        for (int k = 0; k < 5; ++k) W = fma(levt[(6 + k) * T], shfl_up(W, 1 << k), W);
         if (lane == 31) S.sw2[warp] = W;
         __syncthreads();  // barrier 3
-        double v = 0.0;
+        double vw = 0.0;
 #pragma unroll
         for (int w2 = 0; w2 < NW - 1; ++w2)
-          if (w2 < warp) v = fma(S.wa2[w2], v, S.sw2[w2]);
+          if (w2 < warp) vw = fma(S.wa2[w2], vw, S.sw2[w2]);
         const double Wp = shfl_up(W, 1);
-        const double vin = fma(S.lev[11 * T + tid], v, lane == 0 ? 0.0 : Wp);
-        double ul = fma(-n_left, vin, wz[0]);
-        double uh = fma(-nc[H - 1], fma(A2lo, vin, Zl), wz[H]);
-        wz[0] = ul;
-        wz[H] = uh;
+        double in[4];
+        in[0] = fma(levt[11 * T], vw, lane == 0 ? 0.0 : Wp);
+        in[1] = fma(b0, in[0], v[0]);
+        in[2] = fma(b1, in[1], v[1]);
+        in[3] = fma(b2, in[2], v[2]);
 #pragma unroll
-        for (int i = 1; i < H; ++i) {
-          ul = fma(-nc[i - 1], ul, wz[i]);
-          uh = fma(-nc[H + i - 1], uh, wz[H + i]);
-          wz[i] = ul;
-          wz[H + i] = uh;
-        }
+        for (int i = 0; i < Q; ++i)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int row = q * Q + i;
+            const double m = row == 0 ? -n_left : -nc[row - 1];
+            in[q] = fma(m, in[q], wz[row]);
+            wz[row] = in[q];
+          }
       }
       // ================= rz (+|b|^2 at setup), z halos: barrier 4 ===========
       {
-        double rz_loc = 0.0;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int i = 0; i < R; ++i) rz_loc = fma(r[i], wz[i], rz_loc);
-        const double a = warp_allsum(rz_loc);
+        for (int i = 0; i < R; ++i) acc[i / Q] = fma(r[i], wz[i], acc[i / Q]);
+        const double a = warp_allsum((acc[0] + acc[1]) + (acc[2] + acc[3]));
         const double b2 = j == 0 ? warp_allsum(bb) : 0.0;
         if (lane == 0) {
           S.red[2][warp] = a;
@@ -292,11 +387,11 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
         S.zl[tid] = wz[R - 1];
         __syncthreads();  // barrier 4
       }
-      const double rz_next = cross_warp_sum<NW>(S.red[2], lane);
+      const double rz_next = tree_sum<NW>(S.red[2]);
       const double zl_left = tid > 0 ? S.zl[tid - 1] : 0.0;
       const double zf_right = tid < T - 1 ? S.zf[tid + 1] : 0.0;
       if (j == 0) {
-        norm_b = sqrt(cross_warp_sum<NW>(S.red[3], lane));
+        norm_b = sqrt(tree_sum<NW>(S.red[3]));
         if (norm_b == 0.0) {
           st = VQPC_S_CONVERGED;
           break;
@@ -329,23 +424,35 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
         break;
       }
       {
-        double pap_loc = 0.0;
-        double c_lo = S.cs[tid];
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#if VQPC_AP_CSR
+        double c_lo = cst[0];
 #pragma unroll
         for (int i = 0; i < R; ++i) {
-          const double c_hi = i + 1 < R ? S.cs[(i + 1) * T + tid] : S.cs[tid + 1];
+          const double c_hi = i + 1 < R ? cst[(i + 1) * T] : *c_halo;
           const double pl = i == 0 ? p_left : p[i - 1];
-          const double pr = i == R - 1 ? p_right : p[i + 1];
-          const double t = fma(c_hi, pr, c_lo * pl);
-          wz[i] = fma(c_lo + c_hi, p[i], -t);  // (A p)_j, reusing wz
-          pap_loc = fma(p[i], wz[i], pap_loc);
+          const double pr = i + 1 < R ? p[i + 1] : p_right;
+          wz[i] = csr_row(c_lo, dgt[i * T], c_hi, pl, p[i], pr);
+          acc[i / Q] = fma(p[i], wz[i], acc[i / Q]);
           c_lo = c_hi;
         }
-        const double a = warp_allsum(pap_loc);
+#else
+        double c_lo = cst[0];
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const double c_hi = i + 1 < R ? cst[(i + 1) * T] : *c_halo;
+          const double pl = i == 0 ? p_left : p[i - 1];
+          const double pr = i + 1 < R ? p[i + 1] : p_right;
+          wz[i] = fused_row(c_lo, dgt[i * T], c_hi, pl, p[i], pr);  // (A p)_j, reusing wz
+          acc[i / Q] = fma(p[i], wz[i], acc[i / Q]);
+          c_lo = c_hi;
+        }
+#endif
+        const double a = warp_allsum((acc[0] + acc[1]) + (acc[2] + acc[3]));
         if (lane == 0) S.red[0][warp] = a;
         __syncthreads();  // barrier 1
       }
-      const double pAp = cross_warp_sum<NW>(S.red[0], lane);
+      const double pAp = tree_sum<NW>(S.red[0]);
       if (!(pAp > 0.0)) {
         st = VQPC_S_BREAKDOWN;
         break;
@@ -358,22 +465,9 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
       }
       x_left = fma(alpha, p_left, x_left);
       x_right = fma(alpha, p_right, x_right);
-      // true residual b - A x
-      rr_loc = 0.0;
-      {
-        double c_lo = S.cs[tid];
-#pragma unroll
-        for (int i = 0; i < R; ++i) {
-          const double c_hi = i + 1 < R ? S.cs[(i + 1) * T + tid] : S.cs[tid + 1];
-          const double xl = i == 0 ? x_left : x[i - 1];
-          const double xr = i == R - 1 ? x_right : x[i + 1];
-          const double t = fma(c_hi, xr, c_lo * xl);
-          double rt = prm.h - fma(c_lo + c_hi, x[i], -t);
-          if (tail_thread && j0 + i >= n) rt = 0.0;
-          rr_loc = fma(rt, rt, rr_loc);
-          c_lo = c_hi;
-        }
-      }
+      // true residual b - A x; dead rows (b_j = 0) only exist in the last warp
+      rr_loc = warp == NW - 1 ? true_residual<R, T, true>(x, x_left, x_right, cst, dgt, c_halo, prm.h, j0, n)
+                              : true_residual<R, T, false>(x, x_left, x_right, cst, dgt, c_halo, prm.h, j0, n);
     }
 
     if (tid == 0) {

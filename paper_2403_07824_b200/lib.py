@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libvqpc.so")
+LIB_PATH = os.environ.get("VQPC_LIB", os.path.join(HERE, "libvqpc.so"))
 
 METHODS = {"kmeans": 0, "clvq": 1, "grid": 2, "sign_grid": 3}
 MAPS = {"scale": 0, "cdf": 1}
