@@ -68,6 +68,7 @@ enum vqpc_sample_status {
   VQPC_S_COEFF_OVERFLOW = 3,    /* transport produced a non-finite kappa */
   VQPC_S_INVALID_LATENT = 4,    /* non-finite xi */
   VQPC_S_INVALID_COEFF = 5,
+  VQPC_S_NOT_SOLVED = 6,        /* realised + assigned only (beyond solve_limit) */
 };
 
 enum vqpc_method { VQPC_KMEANS = 0, VQPC_CLVQ = 1, VQPC_GRID = 2, VQPC_SIGN_GRID = 3 };
@@ -149,6 +150,15 @@ int vqpc_run_campaign(vqpc_ctx* ctx, const double* xi, int64_t B, int ld, double
 int vqpc_run_campaign_d(vqpc_ctx* ctx, const double* d_xi, int64_t B, int ld, double eps, int max_iter,
                         int64_t chunk, int32_t* d_labels, int32_t* d_iters, double* d_final_rel,
                         uint8_t* d_status, int64_t* d_stats, int64_t* d_summary);
+/* Same, realising and assigning all B samples but solving only those with
+ * index < solve_limit (BASELINE C5: 2^20 realised/assigned, 2^16 solved);
+ * the others get status VQPC_S_NOT_SOLVED and are excluded from the stats. */
+int vqpc_run_campaign_ex(vqpc_ctx* ctx, const double* xi, int64_t B, int ld, double eps, int max_iter,
+                         int64_t chunk, int64_t solve_limit, int32_t* labels, int32_t* iters,
+                         double* final_rel, uint8_t* status, int64_t* stats, int64_t* summary);
+int vqpc_run_campaign_ex_d(vqpc_ctx* ctx, const double* d_xi, int64_t B, int ld, double eps, int max_iter,
+                           int64_t chunk, int64_t solve_limit, int32_t* d_labels, int32_t* d_iters,
+                           double* d_final_rel, uint8_t* d_status, int64_t* d_stats, int64_t* d_summary);
 
 /* ---- per-kernel device timing (CUDA events on the context's stream) ------
  * enable != 0 brackets every kernel launch with events; vqpc_profile_read

@@ -195,7 +195,8 @@ def run_campaign_with(cfg, artifacts, xi, ctx=None, chunk=None):
     if own:
         ctx = make_context(cfg, artifacts)
     try:
-        res = ctx.run_campaign(xi, cfg["eps"], -1, cfg.get("chunk", 0) if chunk is None else chunk)
+        res = ctx.run_campaign(xi, cfg["eps"], -1, cfg.get("chunk", 0) if chunk is None else chunk,
+                               cfg.get("solve_subset", -1))
     finally:
         if own:
             ctx.close()

@@ -46,12 +46,21 @@
 // all threads hold identical bits and the order never depends on scheduling.
 // Breakdown checks use !(v > 0) exactly like the reference (NaN-safe).
 //
+// Cluster variant (CL = 2, n up to 2 R T): a sample spans the two CTAs of a
+// thread-block cluster (one per SM); warp aggregates, reduction partials and
+// the CTA-boundary z halos go through distributed shared memory and the four
+// per-iteration barriers become cluster barriers. Every CTA still folds the
+// same NWT = CL * NW warp values in the same order, so results are identical
+// to a single-CTA run of the same rows.
+//
 // Dead rows j >= n: n_j = 1/u_j^2 = 0 (so z_j = p_j = x_j = 0), n_{n-1} = 0,
 // d_j = 0 and the coupling c_j = 0 for j >= n (the diagonal of row n-1 keeps the
 // true c_n), so (A v)_j = 0 on dead rows without any masking; only b_j = 0 is
 // special, so the residual of the last warp (the only one that can own dead
 // rows) takes a masked code path behind a warp-uniform branch.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace vqpc {
@@ -69,6 +78,7 @@ struct Pcg1dParams {
   int NP;                     // padded rows per factor (= R*T)
   int64_t B;                  // samples in this batch
   int64_t out_base;           // global index of local sample 0 (outputs)
+  int64_t solve_limit;        // samples with global index >= this are not solved
   double eps;
   int max_iter;               // < 0 -> 10 n
   const int32_t* max_iter_arr;  // nullable, indexed by global sample
@@ -79,20 +89,21 @@ struct Pcg1dParams {
   double* x_out;              // nullable, (global sample) x n
 };
 
-template <int R, int T>
+template <int R, int T, int CL>
 struct Pcg1dShared {
   static constexpr int NW = T / 32;
+  static constexpr int NWT = CL * NW;  // warps per sample (whole cluster)
   double2 fac[R * T];     // {n_j, 1/u_j^2}, thread-major
   double cs[R * T];       // coupling c_j = kappa_j / h (0 for j >= n), thread-major
   double dg[R * T];       // diagonal d_j = c_j + c_{j+1} (true c_n; 0 for dead rows)
   double cs_end;          // c_{R*T}: right coupling of the last thread's last row
   double lev[12 * T];     // per-thread lane-scan multipliers: L1[5], Q1, L2[5], Q2
   double qa[8 * T];       // per-thread quarter products: sweep 1 [0..3], sweep 2 [4..7]
-  double wa1[NW], wa2[NW];  // per-warp products of the sweep multipliers
-  double sw1[NW], sw2[NW];  // per-iteration warp aggregates
-  double red[4][NW];        // reduction partials: pAp, rr, rz, |b|^2
+  double wa1[NWT], wa2[NWT];  // per-warp products of the sweep multipliers (all CTAs)
+  double sw1[NWT], sw2[NWT];  // per-iteration warp aggregates (all CTAs)
+  double red[4][NWT];         // reduction partials: pAp, rr, rz, |b|^2 (all CTAs)
   double zf[T], zl[T];      // first / last z of every thread
-  int item;
+  int64_t item;
 };
 
 // The true residual b - A x decides J (rel < eps), so it is evaluated in the
@@ -170,17 +181,36 @@ __device__ __forceinline__ double tree_sum(const double* part) {
   return v[0];
 }
 
-template <int R, int T>
+template <int R, int T, int CL>
 __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
-  using Sh = Pcg1dShared<R, T>;
+  using Sh = Pcg1dShared<R, T, CL>;
   constexpr int NW = Sh::NW;
+  constexpr int NWT = Sh::NWT;
   constexpr int Q = R / 4;  // rows per quarter chain
   static_assert(R % 4 == 0 && R >= 4, "four quarter-chains per thread");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Sh& S = *reinterpret_cast<Sh*>(smem_raw);
 
+  namespace cg = cooperative_groups;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int j0 = tid * R;
+  const int rank = CL == 1 ? 0 : static_cast<int>(cg::this_cluster().block_rank());
+  const int gwarp = rank * NW + warp;  // warp index within the sample
+  const int j0 = (rank * T + tid) * R;  // first row of this thread
+  // peer CTA's shared struct (CL == 2); same layout at the same offset
+  Sh* peer = &S;
+  if constexpr (CL == 2) peer = cg::this_cluster().map_shared_rank(&S, rank ^ 1);
+  auto bar = [&]() {
+    if constexpr (CL == 1)
+      __syncthreads();
+    else
+      cg::this_cluster().sync();
+  };
+  // write a cross-warp value into every CTA of the cluster
+  auto publish = [&](double* local_arr, int idx, double v) {
+    local_arr[idx] = v;
+    if constexpr (CL == 2) reinterpret_cast<double*>(reinterpret_cast<char*>(peer) +
+                                                     (reinterpret_cast<char*>(local_arr) - reinterpret_cast<char*>(&S)))[idx] = v;
+  };
   const int n = prm.n;
   const double* cst = S.cs + tid;      // cst[i*T] = c_{j0+i}
   const double* levt = S.lev + tid;    // levt[k*T]
@@ -194,30 +224,36 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
   double n_left = 0.0;  // n_{j0-1}
 
   for (;;) {
-    if (tid == 0) S.item = atomicAdd(prm.counter, 1);
-    __syncthreads();
+    if (rank == 0 && tid == 0) {
+      const int64_t it = atomicAdd(prm.counter, 1);
+      S.item = it;
+      if constexpr (CL == 2) peer->item = it;
+    }
+    bar();
     const int64_t item = S.item;
-    __syncthreads();
+    bar();
     if (item >= prm.B) break;
     const int s = prm.perm[item];
     const int64_t gs = prm.out_base + s;
     const int label = prm.labels[s];
-    if (label < 0 || prm.kflag[s]) {
-      if (tid == 0) {
+    if (label < 0 || prm.kflag[s] || gs >= prm.solve_limit) {
+      if (rank == 0 && tid == 0) {
         prm.iters[gs] = 0;
         prm.rel[gs] = 0.0;
-        prm.status[gs] = label < 0 ? VQPC_S_INVALID_LATENT : VQPC_S_COEFF_OVERFLOW;
+        prm.status[gs] = gs >= prm.solve_limit ? VQPC_S_NOT_SOLVED
+                         : label < 0           ? VQPC_S_INVALID_LATENT
+                                               : VQPC_S_COEFF_OVERFLOW;
       }
       continue;
     }
     if (label != cur_label) {
       // ---- new bucket: factor to smem, per-thread / per-lane scan constants ----
-      const double2* src = prm.factors + static_cast<size_t>(label) * prm.NP;
+      const double2* src = prm.factors + static_cast<size_t>(label) * prm.NP + static_cast<size_t>(rank) * R * T;
       for (int e = tid; e < R * T; e += T) S.fac[(e % R) * T + e / R] = src[e];  // coalesced read
       __syncthreads();
 #pragma unroll
       for (int i = 0; i < R; ++i) nc[i] = fact[i * T].x;
-      n_left = tid > 0 ? S.fac[(R - 1) * T + tid - 1].x : 0.0;
+      n_left = tid > 0 ? S.fac[(R - 1) * T + tid - 1].x : (j0 > 0 ? src[-1].x : 0.0);
       double P1 = 1.0, P2 = 1.0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -245,8 +281,8 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
       const double q1 = shfl_down(P1, 1), q2 = shfl_up(P2, 1);
       S.lev[5 * T + tid] = lane < 31 ? q1 : 1.0;
       S.lev[11 * T + tid] = lane > 0 ? q2 : 1.0;
-      if (lane == 0) S.wa1[warp] = P1;
-      if (lane == 31) S.wa2[warp] = P2;
+      if (lane == 0) publish(S.wa1, gwarp, P1);
+      if (lane == 31) publish(S.wa2, gwarp, P2);
       cur_label = label;
       __syncthreads();
     }
@@ -264,7 +300,8 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
         S.dg[i * T + tid] = j < n ? __dadd_rn(c_prev, c_next) : 0.0;
         c_prev = c_next;
       }
-      if (tid == T - 1) S.cs_end = 0.0;  // row R*T is never live
+      // right coupling of this CTA's last row: c_{j0+R} (0 beyond the live rows)
+      if (tid == T - 1) S.cs_end = j0 + R < n ? kap[j0 + R] / prm.h : 0.0;
     }
     double x[R], r[R], p[R], wz[R];
     double bbq[4] = {0.0, 0.0, 0.0, 0.0};
@@ -301,14 +338,14 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
         for (int k = 0; k < 5; ++k) W = fma(levt[k * T], shfl_down(W, 1 << k), W);
         const double rrw = warp_allsum(rr_loc);
         if (lane == 0) {
-          S.sw1[warp] = W;
-          S.red[1][warp] = rrw;
+          publish(S.sw1, gwarp, W);
+          publish(S.red[1], gwarp, rrw);
         }
-        __syncthreads();  // barrier 2
+        bar();  // barrier 2
         double vw = 0.0;
 #pragma unroll
-        for (int w2 = NW - 1; w2 > 0; --w2)
-          if (w2 > warp) vw = fma(S.wa1[w2], vw, S.sw1[w2]);
+        for (int w2 = NWT - 1; w2 > 0; --w2)
+          if (w2 > gwarp) vw = fma(S.wa1[w2], vw, S.sw1[w2]);
         const double Wn = shfl_down(W, 1);
         double in[4];
         in[3] = fma(levt[5 * T], vw, lane == 31 ? 0.0 : Wn);
@@ -326,7 +363,7 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
         for (int i = 0; i < R; ++i) wz[i] *= fact[i * T].y;
       }
       if (j > 0) {
-        const double rr = tree_sum<NW>(S.red[1]);
+        const double rr = tree_sum<NWT>(S.red[1]);
         const double rel = sqrt(rr) / norm_b;
         J = j;
         rel_rec = rel;
@@ -350,12 +387,12 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
         W = fma(b3, W, v[3]);
 #pragma unroll
         for (int k = 0; k < 5; ++k) W = fma(levt[(6 + k) * T], shfl_up(W, 1 << k), W);
-        if (lane == 31) S.sw2[warp] = W;
-        __syncthreads();  // barrier 3
+        if (lane == 31) publish(S.sw2, gwarp, W);
+        bar();  // barrier 3
         double vw = 0.0;
 #pragma unroll
-        for (int w2 = 0; w2 < NW - 1; ++w2)
-          if (w2 < warp) vw = fma(S.wa2[w2], vw, S.sw2[w2]);
+        for (int w2 = 0; w2 < NWT - 1; ++w2)
+          if (w2 < gwarp) vw = fma(S.wa2[w2], vw, S.sw2[w2]);
         const double Wp = shfl_up(W, 1);
         double in[4];
         in[0] = fma(levt[11 * T], vw, lane == 0 ? 0.0 : Wp);
@@ -380,18 +417,19 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
         const double a = warp_allsum((acc[0] + acc[1]) + (acc[2] + acc[3]));
         const double b2 = j == 0 ? warp_allsum(bb) : 0.0;
         if (lane == 0) {
-          S.red[2][warp] = a;
-          S.red[3][warp] = b2;
+          publish(S.red[2], gwarp, a);
+          publish(S.red[3], gwarp, b2);
         }
         S.zf[tid] = wz[0];
         S.zl[tid] = wz[R - 1];
-        __syncthreads();  // barrier 4
+        bar();  // barrier 4
       }
-      const double rz_next = tree_sum<NW>(S.red[2]);
-      const double zl_left = tid > 0 ? S.zl[tid - 1] : 0.0;
-      const double zf_right = tid < T - 1 ? S.zf[tid + 1] : 0.0;
+      const double rz_next = tree_sum<NWT>(S.red[2]);
+      // z halos; across the CTA boundary they are read from the peer (DSMEM)
+      const double zl_left = tid > 0 ? S.zl[tid - 1] : (CL == 2 && rank == 1 ? peer->zl[T - 1] : 0.0);
+      const double zf_right = tid < T - 1 ? S.zf[tid + 1] : (CL == 2 && rank == 0 ? peer->zf[0] : 0.0);
       if (j == 0) {
-        norm_b = sqrt(tree_sum<NW>(S.red[3]));
+        norm_b = sqrt(tree_sum<NWT>(S.red[3]));
         if (norm_b == 0.0) {
           st = VQPC_S_CONVERGED;
           break;
@@ -449,10 +487,10 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
         }
 #endif
         const double a = warp_allsum((acc[0] + acc[1]) + (acc[2] + acc[3]));
-        if (lane == 0) S.red[0][warp] = a;
-        __syncthreads();  // barrier 1
+        if (lane == 0) publish(S.red[0], gwarp, a);
+        bar();  // barrier 1
       }
-      const double pAp = tree_sum<NW>(S.red[0]);
+      const double pAp = tree_sum<NWT>(S.red[0]);
       if (!(pAp > 0.0)) {
         st = VQPC_S_BREAKDOWN;
         break;
@@ -466,11 +504,11 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
       x_left = fma(alpha, p_left, x_left);
       x_right = fma(alpha, p_right, x_right);
       // true residual b - A x; dead rows (b_j = 0) only exist in the last warp
-      rr_loc = warp == NW - 1 ? true_residual<R, T, true>(x, x_left, x_right, cst, dgt, c_halo, prm.h, j0, n)
+      rr_loc = gwarp == NWT - 1 ? true_residual<R, T, true>(x, x_left, x_right, cst, dgt, c_halo, prm.h, j0, n)
                               : true_residual<R, T, false>(x, x_left, x_right, cst, dgt, c_halo, prm.h, j0, n);
     }
 
-    if (tid == 0) {
+    if (rank == 0 && tid == 0) {
       prm.iters[gs] = J;
       prm.rel[gs] = rel_rec;
       prm.status[gs] = st;
@@ -482,11 +520,12 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
         if (j0 + i < n) xo[j0 + i] = x[i];
     }
   }
+  if constexpr (CL == 2) cg::this_cluster().sync();  // no CTA exits while its peer may read its smem
 }
 
-template <int R, int T>
+template <int R, int T, int CL>
 constexpr size_t pcg1d_smem_bytes() {
-  return sizeof(Pcg1dShared<R, T>);
+  return sizeof(Pcg1dShared<R, T, CL>);
 }
 
 }  // namespace vqpc

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
+#include <cstdint>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -151,21 +153,23 @@ struct Timed {
 // ---- pcg variant table: rows per thread R, threads T (n <= R*T) ------------
 using PcgFn = void (*)(const Pcg1dParams);
 struct PcgVariant {
-  int R, T;
+  int R, T, CL;
   PcgFn fn;
   size_t smem;
 };
 
-template <int R, int T>
+template <int R, int T, int CL>
 PcgVariant make_variant() {
-  return PcgVariant{R, T, &pcg1d_kernel<R, T>, pcg1d_smem_bytes<R, T>()};
+  return PcgVariant{R, T, CL, &pcg1d_kernel<R, T, CL>, pcg1d_smem_bytes<R, T, CL>()};
 }
 
+// smallest variant whose R*T*CL rows hold the n unknowns; n <= 4096 fits one SM's
+// register file (one CTA per sample), n <= 8192 uses a 2-CTA cluster
 const PcgVariant* pick_pcg(int n) {
-  static const PcgVariant table[] = {
-      make_variant<16, 64>(), make_variant<16, 128>(), make_variant<16, 256>(), make_variant<16, 512>()};
+  static const PcgVariant table[] = {make_variant<16, 64, 1>(), make_variant<16, 128, 1>(),
+                                     make_variant<16, 256, 1>(), make_variant<16, 256, 2>()};
   for (const auto& v : table)
-    if (n <= v.R * v.T) return &v;
+    if (n <= v.R * v.T * v.CL) return &v;
   return nullptr;
 }
 
@@ -241,7 +245,8 @@ void run_bucket(vqpc_ctx* c, const int32_t* d_labels, int64_t B, int32_t* d_perm
 
 void run_pcg(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d_kflag, const int32_t* d_perm,
              const int32_t* d_labels, int64_t B, int64_t out_base, double eps, int max_iter, const int32_t* d_mia,
-             int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x) {
+             int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x,
+             int64_t solve_limit = INT64_MAX) {
   if (B <= 0) return;
   if (c->pb.dim != 1) throw ApiError{VQPC_INVALID_CONFIG, "2-D solve path not built in this version"};
   const PcgVariant* v = pick_pcg(c->n);
@@ -260,6 +265,7 @@ void run_pcg(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d_k
   prm.NP = c->NP;
   prm.B = B;
   prm.out_base = out_base;
+  prm.solve_limit = solve_limit;
   prm.eps = eps;
   prm.max_iter = max_iter;
   prm.max_iter_arr = d_mia;
@@ -269,12 +275,33 @@ void run_pcg(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d_k
   prm.status = d_status;
   prm.x_out = d_x;
   CK(cudaFuncSetAttribute(v->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(v->smem)));
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v->fn, v->T, v->smem));
-  if (per_sm < 1) throw ApiError{VQPC_CUDA_ERROR, "pcg kernel does not fit on an SM"};
-  const int64_t grid = std::min<int64_t>(B, static_cast<int64_t>(per_sm) * c->sm_count);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  cfg.blockDim = dim3(v->T);
+  cfg.dynamicSmemBytes = v->smem;
+  cfg.stream = c->stream;
+  int64_t groups = 0;  // concurrently resident samples (CTAs or clusters)
+  if (v->CL == 1) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v->fn, v->T, v->smem));
+    groups = static_cast<int64_t>(per_sm) * c->sm_count;
+  } else {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = v->CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(static_cast<unsigned>(v->CL * c->sm_count));
+    int clusters = 0;
+    CK(cudaOccupancyMaxActiveClusters(&clusters, v->fn, &cfg));
+    groups = clusters;
+  }
+  if (groups < 1) throw ApiError{VQPC_CUDA_ERROR, "pcg kernel does not fit on the device"};
+  groups = std::min<int64_t>(B, groups);
+  cfg.gridDim = dim3(static_cast<unsigned>(groups * v->CL));
   Timed tm(c, VQPC_K_PCG);
-  v->fn<<<static_cast<unsigned>(grid), v->T, v->smem, c->stream>>>(prm);
+  CK(cudaLaunchKernelEx(&cfg, v->fn, prm));
   launch_check(c);
 }
 
@@ -283,6 +310,7 @@ __global__ void stats_kernel(const int32_t* labels, const int32_t* iters, const 
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= B) return;
   const int l = labels[i];
+  if (status[i] == VQPC_S_NOT_SOLVED) return;
   const unsigned long long J = static_cast<unsigned long long>(iters[i]);
   const bool conv = status[i] == VQPC_S_CONVERGED;
   atomicAdd(&summary[0], J);
@@ -295,6 +323,14 @@ __global__ void stats_kernel(const int32_t* labels, const int32_t* iters, const 
     atomicAdd(&stats[2 * P + l], 1ull);
     atomicAdd(&stats[3 * P + l], J);
   }
+}
+
+__global__ void mark_unsolved_kernel(int32_t* iters, double* rel, uint8_t* status, int64_t B) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= B) return;
+  iters[i] = 0;
+  rel[i] = 0.0;
+  status[i] = VQPC_S_NOT_SOLVED;
 }
 
 template <class F>
@@ -329,7 +365,7 @@ int64_t kappa_ld(const vqpc_ctx* c) { return (c->pb.n_nodes + 1) & ~1; }
 // The full campaign on device-resident arrays (run_campaign_with semantics).
 void campaign_device(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, double eps, int max_iter, int64_t chunk,
                      int32_t* d_labels, int32_t* d_iters, double* d_rel, uint8_t* d_status, int64_t* d_stats,
-                     int64_t* d_summary) {
+                     int64_t* d_summary, int64_t solve_limit = INT64_MAX) {
   if (!(eps > 0.0) || eps >= 1.0) throw ApiError{VQPC_INVALID_TOLERANCE, "invalid-tolerance"};
   if (ld < c->pb.n_kl) throw ApiError{VQPC_INVALID_ARGUMENT, "ld < n_kl"};
   if (!c->factored) throw ApiError{VQPC_INVALID_CONFIG, "vqpc_factor_centroids must precede solves"};
@@ -348,8 +384,14 @@ void campaign_device(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, double 
     run_bucket(c, d_labels + c0, nb, c->perm.p, c->offsets.p);
     CK(cudaMemsetAsync(c->kflag.p, 0, nb, c->stream));
     run_realise(c, xi, nb, ld, c->pb.n_kl, c->kappa.p, ldk, c->kflag.p);
+    if (c0 >= solve_limit) {  // whole chunk beyond the solve subset: mark, skip the solver
+      mark_unsolved_kernel<<<static_cast<unsigned>(ceil_div(nb, 256)), 256, 0, c->stream>>>(
+          d_iters + c0, d_rel + c0, d_status + c0, nb);
+      launch_check(c);
+      continue;
+    }
     run_pcg(c, c->kappa.p, ldk, c->kflag.p, c->perm.p, d_labels + c0, nb, c0, eps, max_iter, nullptr, d_iters,
-            d_rel, d_status, nullptr);
+            d_rel, d_status, nullptr, solve_limit);
   }
   CK(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 4 * P, c->stream));
   CK(cudaMemsetAsync(d_summary, 0, sizeof(int64_t) * 4, c->stream));
@@ -417,7 +459,7 @@ int vqpc_ctx_create(const vqpc_problem* pb, vqpc_ctx** out) {
       if (!v) throw ApiError{VQPC_INVALID_CONFIG, "1-D system larger than the largest pcg variant"};
       c->pcgR = v->R;
       c->pcgT = v->T;
-      c->NP = v->R * v->T;
+      c->NP = v->R * v->T * v->CL;
     }
     const size_t K = pb->n_kl, nn = pb->n_nodes;
     std::vector<double> sl(K);
@@ -682,17 +724,25 @@ int vqpc_profile_read(vqpc_ctx* c, double* ms, int64_t* counts, int reset) {
   });
 }
 
-int vqpc_run_campaign_d(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, double eps, int max_iter, int64_t chunk,
-                        int32_t* d_labels, int32_t* d_iters, double* d_rel, uint8_t* d_status, int64_t* d_stats,
-                        int64_t* d_summary) {
+int vqpc_run_campaign_ex_d(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, double eps, int max_iter,
+                           int64_t chunk, int64_t solve_limit, int32_t* d_labels, int32_t* d_iters, double* d_rel,
+                           uint8_t* d_status, int64_t* d_stats, int64_t* d_summary) {
   if (!c) return VQPC_INVALID_ARGUMENT;
   return guard(c, [&] {
-    campaign_device(c, d_xi, B, ld, eps, max_iter, chunk, d_labels, d_iters, d_rel, d_status, d_stats, d_summary);
+    campaign_device(c, d_xi, B, ld, eps, max_iter, chunk, d_labels, d_iters, d_rel, d_status, d_stats, d_summary,
+                    solve_limit < 0 ? INT64_MAX : solve_limit);
   });
 }
 
-int vqpc_run_campaign(vqpc_ctx* c, const double* xi, int64_t B, int ld, double eps, int max_iter, int64_t chunk,
-                      int32_t* labels, int32_t* iters, double* final_rel, uint8_t* status, int64_t* stats,
+int vqpc_run_campaign_d(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, double eps, int max_iter, int64_t chunk,
+                        int32_t* d_labels, int32_t* d_iters, double* d_rel, uint8_t* d_status, int64_t* d_stats,
+                        int64_t* d_summary) {
+  return vqpc_run_campaign_ex_d(c, d_xi, B, ld, eps, max_iter, chunk, -1, d_labels, d_iters, d_rel, d_status,
+                                d_stats, d_summary);
+}
+
+int vqpc_run_campaign_ex(vqpc_ctx* c, const double* xi, int64_t B, int ld, double eps, int max_iter, int64_t chunk,
+                         int64_t solve_limit, int32_t* labels, int32_t* iters, double* final_rel, uint8_t* status, int64_t* stats,
                       int64_t* summary) {
   if (!c) return VQPC_INVALID_ARGUMENT;
   return guard(c, [&] {
@@ -706,7 +756,7 @@ int vqpc_run_campaign(vqpc_ctx* c, const double* xi, int64_t B, int ld, double e
     c->stats.ensure(4 * static_cast<size_t>(P) + 4);
     h2d(c, c->xi.p, xi, static_cast<size_t>(B) * ld);
     campaign_device(c, c->xi.p, B, ld, eps, max_iter, chunk, c->labels.p, c->iters.p, c->rel.p, c->status.p,
-                    c->stats.p, c->stats.p + 4 * P);
+                    c->stats.p, c->stats.p + 4 * P, solve_limit < 0 ? INT64_MAX : solve_limit);
     d2h(c, labels, c->labels.p, B);
     d2h(c, iters, c->iters.p, B);
     d2h(c, final_rel, c->rel.p, B);
@@ -715,6 +765,13 @@ int vqpc_run_campaign(vqpc_ctx* c, const double* xi, int64_t B, int ld, double e
     d2h(c, summary, c->stats.p + 4 * P, 4);
     CK(cudaStreamSynchronize(c->stream));
   });
+}
+
+int vqpc_run_campaign(vqpc_ctx* c, const double* xi, int64_t B, int ld, double eps, int max_iter, int64_t chunk,
+                      int32_t* labels, int32_t* iters, double* final_rel, uint8_t* status, int64_t* stats,
+                      int64_t* summary) {
+  return vqpc_run_campaign_ex(c, xi, B, ld, eps, max_iter, chunk, -1, labels, iters, final_rel, status, stats,
+                              summary);
 }
 
 }  // extern "C"

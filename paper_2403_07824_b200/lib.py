@@ -17,7 +17,7 @@ METHODS = {"kmeans": 0, "clvq": 1, "grid": 2, "sign_grid": 3}
 MAPS = {"scale": 0, "cdf": 1}
 PRECONDS = {"identity": 0, "cholesky": 1, "ic0": 4}
 STATUS = {0: "converged", 1: "max_iter", 2: "breakdown", 3: "coefficient-overflow", 4: "invalid-latent",
-          5: "invalid-coefficient"}
+          5: "invalid-coefficient", 6: "not-solved"}
 
 
 class VqpcError(RuntimeError):
@@ -64,6 +64,8 @@ def load():
             "vqpc_solve_batch": (I, [VP, VP, I64, I, VP, D, I, VP, VP, VP, VP, VP]),
             "vqpc_run_campaign": (I, [VP, VP, I64, I, D, I, I64, VP, VP, VP, VP, VP, VP]),
             "vqpc_run_campaign_d": (I, [VP, VP, I64, I, D, I, I64, VP, VP, VP, VP, VP, VP]),
+            "vqpc_run_campaign_ex": (I, [VP, VP, I64, I, D, I, I64, I64, VP, VP, VP, VP, VP, VP]),
+            "vqpc_run_campaign_ex_d": (I, [VP, VP, I64, I, D, I, I64, I64, VP, VP, VP, VP, VP, VP]),
             "vqpc_kmeans": (I, [I, VP, I, I, VP, I, I, U64, I, D, VP, VP, C.POINTER(C.c_int)]),
             "vqpc_draw_standard_normal": (I, [I64, I, U64, I64, VP, I]),
             "vqpc_profile": (I, [VP, I]),
@@ -242,8 +244,9 @@ class Context:
                                         _p(st), _p(x)))
         return it, rel, st, x
 
-    def run_campaign(self, xi, eps, max_iter=-1, chunk=0):
-        """run_campaign_with (driver.cpp:193-281) on host arrays (copies included)."""
+    def run_campaign(self, xi, eps, max_iter=-1, chunk=0, solve_limit=-1):
+        """run_campaign_with (driver.cpp:193-281) on host arrays (copies included);
+        solve_limit >= 0 solves only the first solve_limit samples (C5)."""
         xi = f64(xi)
         B, ld = xi.shape
         P = self.P
@@ -253,15 +256,16 @@ class Context:
         st = np.empty(B, np.uint8)
         stats = np.empty(4 * P, np.int64)
         summary = np.empty(4, np.int64)
-        self._c(load().vqpc_run_campaign(self.h, _p(xi), B, ld, eps, max_iter, chunk, _p(labels), _p(it), _p(rel),
-                                         _p(st), _p(stats), _p(summary)))
+        self._c(load().vqpc_run_campaign_ex(self.h, _p(xi), B, ld, eps, max_iter, chunk, solve_limit, _p(labels),
+                                            _p(it), _p(rel), _p(st), _p(stats), _p(summary)))
         return dict(labels=labels, iterations=it, rel=rel, status=st, n_p=stats[:P], sum_j=stats[P:2 * P],
                     conv_count=stats[2 * P:3 * P], conv_sum=stats[3 * P:], total_iterations=int(summary[0]),
                     unconverged=int(summary[1]), conv_total=int(summary[2]), conv_sum_total=int(summary[3]))
 
     def run_campaign_device(self, d_xi_ptr, B, ld, eps, d_labels, d_iters, d_rel, d_status, d_stats, d_summary,
-                            max_iter=-1, chunk=0):
+                            max_iter=-1, chunk=0, solve_limit=-1):
         """Device-resident variant: every argument is a raw device pointer (int)."""
         V = C.c_void_p
-        self._c(load().vqpc_run_campaign_d(self.h, V(d_xi_ptr), B, ld, eps, max_iter, chunk, V(d_labels), V(d_iters),
-                                           V(d_rel), V(d_status), V(d_stats), V(d_summary)))
+        self._c(load().vqpc_run_campaign_ex_d(self.h, V(d_xi_ptr), B, ld, eps, max_iter, chunk, solve_limit,
+                                              V(d_labels), V(d_iters), V(d_rel), V(d_status), V(d_stats),
+                                              V(d_summary)))

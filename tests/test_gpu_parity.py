@@ -23,7 +23,7 @@ def test_kmeans_bit_identical(name, n_real, ns):
     assert np.array_equal(h_gpu, h_cpu)
 
 
-@pytest.mark.parametrize("name,n_real", [("C1", 4096), ("C2", 8192), ("C3", 8192)])
+@pytest.mark.parametrize("name,n_real", [("C1", 4096), ("C2", 8192), ("C3", 8192), ("C5", 3072)])
 def test_assign_bit_exact(name, n_real):
     cfg, basis, cb, xi = setup_case(name, n_real)
     ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb), factor=False)
@@ -32,7 +32,7 @@ def test_assign_bit_exact(name, n_real):
     assert np.array_equal(lab_gpu, lab_cpu)
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C5"])
 def test_realise_matches_lift_transport(name):
     cfg, basis, cb, xi = setup_case(name, 300)
     ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb), factor=False)
@@ -43,7 +43,7 @@ def test_realise_matches_lift_transport(name):
     assert rel.max() < 1e-13, rel.max()
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C5"])
 def test_centroid_factor_apply(name):
     cfg, basis, cb, xi = setup_case(name, 64)
     ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
@@ -123,7 +123,7 @@ def test_campaign_C1_full():
     assert cmp["n_both"] > 4000
 
 
-@pytest.mark.parametrize("name,n_real", [("C2", 1024), ("C3", 1024)])
+@pytest.mark.parametrize("name,n_real", [("C2", 1024), ("C3", 1024), ("C5", 192)])
 def test_campaign_subsets(name, n_real):
     _check_j_parity(name, n_real)
 
@@ -134,14 +134,14 @@ def _fixed_k_x(pset, basis, xi, labels, K, want_x=True):
     return x
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C5"])
 def test_fixed_K_solutions(name):
     """Appendix B.5: both sides run exactly K = min(J_cpu, J_gpu) iterations
     (eps = 1e-300, max_iter = K) and x must agree to 1e-10 in relative l2.
     Yardstick: the same comparison between the oracle and its FMA-contracted
     build; the GPU must be at least as close as that rounding-level variant of
     the reference wherever 1e-10 is not met."""
-    cfg, basis, cb, xi = setup_case(name, 96)
+    cfg, basis, cb, xi = setup_case(name, 96 if name != "C5" else 48)
     ocb = oracle_codebook(cb)
     labels = oracle.assign(ocb, xi)
     L, V = basis["eigenvalues"], basis["eigenvectors"]
@@ -180,6 +180,30 @@ def test_exact_factor_gives_one_iteration(name):
     labels = np.arange(cb["P"], dtype=np.int32)
     it, rel, st, _ = ctx.solve_batch(xi, labels, cfg["eps"])
     assert (st == 0).all() and (it == 1).all(), (it, st)
+
+
+def test_kmeans_bit_identical_m64():
+    """The C5 shape (m = 64) on a CPU-affordable pilot: GPU sweeps == oracle Lloyd."""
+    rs = np.random.default_rng(64)
+    lam = np.sort(rs.uniform(1e-6, 0.2, 64))[::-1].copy()
+    pilot = lib.draw_standard_normal(4096, 64, 1)
+    c_gpu, h_gpu = lib.kmeans(pilot, lam, 128, max_iter=25)
+    c_cpu, h_cpu = oracle.kmeans(pilot, lam, 128, max_iter=25)
+    assert np.array_equal(c_gpu, c_cpu) and np.array_equal(h_gpu, h_cpu)
+
+
+def test_c5_solve_subset_and_chunks():
+    """C5 semantics: all samples realised + assigned in 2^14-style chunks, only the
+    first solve_subset solved; chunking does not change any per-sample result."""
+    cfg, basis, cb, xi = setup_case("C5", 600)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    a = ctx.run_campaign(xi, cfg["eps"], chunk=200, solve_limit=256)
+    assert (a["status"][256:] == 6).all() and (a["status"][:256] != 6).all()
+    assert int(a["n_p"].sum()) == 256
+    b = ctx.run_campaign(xi, cfg["eps"], chunk=0, solve_limit=256)
+    for k in ("labels", "iterations", "rel", "status"):
+        assert np.array_equal(a[k], b[k]), k
+    assert np.array_equal(a["labels"], oracle.assign(oracle_codebook(cb), xi))
 
 
 def test_determinism_across_chunks():
