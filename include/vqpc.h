@@ -105,6 +105,10 @@ const char* vqpc_error_string(int code);
 /* Run all work of this context on an existing cudaStream_t (NULL: own stream). */
 int vqpc_set_stream(vqpc_ctx* ctx, void* cuda_stream);
 int vqpc_synchronize(vqpc_ctx* ctx);
+/* 2-D solver: enable != 0 sums every dot product serially in natural order
+ * (solver.cpp:176-180), making the whole solve bit-identical to the reference
+ * arithmetic at some cost; default 0 = block-tree reductions. No effect in 1-D. */
+int vqpc_set_exact_reductions(vqpc_ctx* ctx, int enable);
 /* unknowns per sample system (n) and the number of device kernel launches
  * issued by this context so far (bench evidence). */
 int vqpc_unknowns(const vqpc_ctx* ctx);

@@ -468,11 +468,26 @@ struct Record {
   uint8_t status = ST_MAX_ITER;
 };
 
-static double dot(const double* a, const double* b, int n) {
+#ifndef VQPO_PAIRWISE_DOT
+static double dot(const double* a, const double* b, int n) {  // solver.cpp:176-180: serial
   double s = 0.0;
   for (int i = 0; i < n; ++i) s += a[i] * b[i];
   return s;
 }
+#else
+// investigation build only (not the oracle): pairwise summation, to measure how
+// much of a GPU/CPU iteration-count difference the summation order explains
+static double dot_rec(const double* a, const double* b, int n) {
+  if (n <= 8) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += a[i] * b[i];
+    return s;
+  }
+  const int h = n / 2;
+  return dot_rec(a, b, h) + dot_rec(a + h, b + h, n - h);
+}
+static double dot(const double* a, const double* b, int n) { return dot_rec(a, b, n); }
+#endif
 
 // Returns the record the reference would hold at exit. A breakdown (where the
 // reference throws "pcg-breakdown") is reported as status ST_BREAKDOWN with the

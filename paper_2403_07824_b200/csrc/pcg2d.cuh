@@ -1,0 +1,529 @@
+// pcg2d.cuh — kernels (e) and (d), 2-D: IC(0) centroid factors and batched PCG
+// on the structured r x r P1 mesh (BASELINE C4: r = 256, 65,025 unknowns).
+//
+// Replaces, per sample, assemble (proj/src/fem.cpp:213-256) + pcg
+// (proj/src/solver.cpp:186-245) with the IC(0) preconditioner of SURVEY
+// Appendix A (not in the reference), and, per centroid, the factorisation
+// step of run_campaign_with (driver.cpp:212-219).
+//
+// Storage: every per-node array lives in HBM in anti-diagonal ("wavefront")
+// order: level l = ix + iy (0 .. 2m-2, m = r-1), nodes of a level contiguous
+// by increasing iy. Thread t of a CTA owns grid row iy = t (T = 256 >= m), so
+// at level l it touches node (l - t, t); its W/S neighbours lie in level l-1
+// and its E/N neighbours in level l+1, so every access of a warp is one
+// coalesced segment.
+//
+// Exactness: the coefficients are assembled in the oracle's insertion order
+// (kbar = ((k_a + k_b) + k_c) / 3, local entries scale * (b_i b_j + c_i c_j),
+// the diagonal summed over the node's six triangles in cell order), the CSR
+// row products use the reference's column order without contraction, and the
+// IC(0) sweeps are level-scheduled: each node performs exactly the sequential
+// sweep's operations on exactly the same inputs. Hence A, b, the IC(0) factor,
+// A v and M^{-1} r are bit-identical to the CPU oracle; only the dot-product
+// summation order differs (block tree vs serial). In exact mode the products
+// are stored at their natural index and summed serially by one thread, and the
+// whole solve (J, residual history, x) is bit-identical to the reference's
+// arithmetic; the tree mode is faster and reproduces the oracle built with
+// pairwise dot products.
+//
+// One CTA per sample (persistent grid, samples in bucket order). Per PCG
+// iteration three passes over the levels:
+//   P1 (barrier-free): p_new = z + beta p_old (ping-pong halves); A p; pAp
+//   P2 (barrier-free): x_new = x_old + alpha p (ping-pong); r -= alpha A p;
+//       r_true = b - A x_new with neighbours' x_new recomputed by the same FMA
+//   P3 (one barrier per level): forward and backward IC(0) sweeps; r.z
+// Ap is recomputed in P2 (bit-identical) instead of stored.
+#pragma once
+#include "common.cuh"
+
+namespace vqpc {
+
+constexpr int P2_T = 256;            // threads per CTA (one per grid row, r <= 257)
+constexpr int P2_MAXL = 2 * P2_T;    // max levels (2m - 1 <= 511)
+
+struct Grid2D {
+  int r;       // mesh resolution
+  int m;       // interior nodes per row (r - 1)
+  int n;       // m * m
+  int L;       // levels 2m - 1
+  double h;    // 1 / r
+};
+
+__host__ __device__ inline int lvl_lo(int l, int m) { return l - (m - 1) > 0 ? l - (m - 1) : 0; }
+__host__ __device__ inline int lvl_hi(int l, int m) { return l < m - 1 ? l : m - 1; }
+
+// ---- coefficient assembly for one interior node, oracle insertion order ------
+// kappa: nodal, (r+1)^2, natural mesh order id = Y (r+1) + X.
+struct RowCoef {
+  double d, w, s, e, nn, b;
+};
+
+__device__ inline void tri_geom(int X0, int Y0, int X1, int Y1, int X2, int Y2, double h, double& area, double bb[3],
+                                double cc[3]) {
+  const double x0 = X0 * h, y0 = Y0 * h, x1 = X1 * h, y1 = Y1 * h, x2 = X2 * h, y2 = Y2 * h;
+  area = __dmul_rn(0.5, __dsub_rn(__dmul_rn(__dsub_rn(x1, x0), __dsub_rn(y2, y0)),
+                                  __dmul_rn(__dsub_rn(x2, x0), __dsub_rn(y1, y0))));
+  bb[0] = __dsub_rn(y1, y2);
+  bb[1] = __dsub_rn(y2, y0);
+  bb[2] = __dsub_rn(y0, y1);
+  cc[0] = __dsub_rn(x2, x1);
+  cc[1] = __dsub_rn(x0, x2);
+  cc[2] = __dsub_rn(x1, x0);
+}
+
+// entry (i, j) of triangle with vertices V[0..2] (mesh coords), i,j local vertex ids
+__device__ inline double tri_entry(const double* kappa, int side, int X[3], int Y[3], int i, int j, double h,
+                                   double* area_out) {
+  double area, bb[3], cc[3];
+  tri_geom(X[0], Y[0], X[1], Y[1], X[2], Y[2], h, area, bb, cc);
+  const double ka = kappa[Y[0] * side + X[0]], kb = kappa[Y[1] * side + X[1]], kc = kappa[Y[2] * side + X[2]];
+  const double kbar = __ddiv_rn(__dadd_rn(__dadd_rn(ka, kb), kc), 3.0);
+  const double scale = __ddiv_rn(kbar, __dmul_rn(4.0, area));
+  if (area_out) *area_out = area;
+  return __dmul_rn(scale, __dadd_rn(__dmul_rn(bb[i], bb[j]), __dmul_rn(cc[i], cc[j])));
+}
+
+// T1 of cell (cx, cy): {a, b, d}; T2: {a, d, c}; a=(cx,cy) b=(cx+1,cy) c=(cx,cy+1) d=(cx+1,cy+1)
+__device__ inline void cell_tri(int cx, int cy, int which, int X[3], int Y[3]) {
+  if (which == 1) {
+    X[0] = cx; Y[0] = cy; X[1] = cx + 1; Y[1] = cy; X[2] = cx + 1; Y[2] = cy + 1;
+  } else {
+    X[0] = cx; Y[0] = cy; X[1] = cx + 1; Y[1] = cy + 1; X[2] = cx; Y[2] = cy + 1;
+  }
+}
+
+// Row of interior node (ix, iy) (mesh node X = ix+1, Y = iy+1): diagonal summed in
+// the oracle's triangle order, couplings as the two-triangle sums, b = area_sum / 3.
+__device__ inline RowCoef assemble_row(const double* kappa, const Grid2D g, int ix, int iy) {
+  const int side = g.r + 1, X = ix + 1, Y = iy + 1;
+  int tx[3], ty[3];
+  double area, diag, asum, e1, e2;
+  // 1) T1(X-1,Y-1): node is d (local 2)
+  cell_tri(X - 1, Y - 1, 1, tx, ty);
+  diag = tri_entry(kappa, side, tx, ty, 2, 2, g.h, &area);
+  asum = area;
+  const double s1 = tri_entry(kappa, side, tx, ty, 2, 1, g.h, nullptr);  // S via T1(X-1,Y-1): (d, b)
+  // 2) T2(X-1,Y-1): node is d (local 1)
+  cell_tri(X - 1, Y - 1, 2, tx, ty);
+  diag = __dadd_rn(diag, tri_entry(kappa, side, tx, ty, 1, 1, g.h, &area));
+  asum = __dadd_rn(asum, area);
+  const double w1 = tri_entry(kappa, side, tx, ty, 1, 2, g.h, nullptr);  // W via T2(X-1,Y-1): (d, c)
+  // 3) T2(X,Y-1): node is c (local 2)
+  cell_tri(X, Y - 1, 2, tx, ty);
+  diag = __dadd_rn(diag, tri_entry(kappa, side, tx, ty, 2, 2, g.h, &area));
+  asum = __dadd_rn(asum, area);
+  const double s2 = tri_entry(kappa, side, tx, ty, 2, 0, g.h, nullptr);  // S via T2(X,Y-1): (c, a)
+  e1 = tri_entry(kappa, side, tx, ty, 2, 1, g.h, nullptr);                // E via T2(X,Y-1): (c, d)
+  // 4) T1(X-1,Y): node is b (local 1)
+  cell_tri(X - 1, Y, 1, tx, ty);
+  diag = __dadd_rn(diag, tri_entry(kappa, side, tx, ty, 1, 1, g.h, &area));
+  asum = __dadd_rn(asum, area);
+  const double w2 = tri_entry(kappa, side, tx, ty, 1, 0, g.h, nullptr);  // W via T1(X-1,Y): (b, a)
+  const double n1 = tri_entry(kappa, side, tx, ty, 1, 2, g.h, nullptr);  // N via T1(X-1,Y): (b, d)
+  // 5) T1(X,Y): node is a (local 0)
+  cell_tri(X, Y, 1, tx, ty);
+  diag = __dadd_rn(diag, tri_entry(kappa, side, tx, ty, 0, 0, g.h, &area));
+  asum = __dadd_rn(asum, area);
+  e2 = tri_entry(kappa, side, tx, ty, 0, 1, g.h, nullptr);  // E via T1(X,Y): (a, b)
+  // 6) T2(X,Y): node is a (local 0)
+  cell_tri(X, Y, 2, tx, ty);
+  diag = __dadd_rn(diag, tri_entry(kappa, side, tx, ty, 0, 0, g.h, &area));
+  asum = __dadd_rn(asum, area);
+  const double n2 = tri_entry(kappa, side, tx, ty, 0, 2, g.h, nullptr);  // N via T2(X,Y): (a, c)
+  RowCoef rc;
+  rc.d = diag;
+  rc.w = ix > 0 ? __dadd_rn(w1, w2) : 0.0;
+  rc.s = iy > 0 ? __dadd_rn(s1, s2) : 0.0;
+  rc.e = ix < g.m - 1 ? __dadd_rn(e1, e2) : 0.0;
+  rc.nn = iy < g.m - 1 ? __dadd_rn(n1, n2) : 0.0;
+  rc.b = __ddiv_rn(asum, 3.0);
+  return rc;
+}
+
+// CSR row product in the reference's column order (S, W, diag, E, N), no contraction
+__device__ __forceinline__ double row_apply(double as, double aw, double d, double ae, double an, double vs, double vw,
+                                            double v, double ve, double vn) {
+  double s = __dmul_rn(as, vs);
+  s = __dadd_rn(s, __dmul_rn(aw, vw));
+  s = __dadd_rn(s, __dmul_rn(d, v));
+  s = __dadd_rn(s, __dmul_rn(ae, ve));
+  return __dadd_rn(s, __dmul_rn(an, vn));
+}
+
+struct LevelTab {
+  int off[P2_MAXL + 2];  // level offsets (off[L] = n)
+  int lo[P2_MAXL + 2];   // smallest iy of each level
+};
+
+__device__ inline void build_levels(LevelTab& tab, const Grid2D g) {
+  if (threadIdx.x == 0) {
+    int off = 0;
+    for (int l = 0; l < g.L; ++l) {
+      tab.off[l] = off;
+      tab.lo[l] = lvl_lo(l, g.m);
+      off += lvl_hi(l, g.m) - tab.lo[l] + 1;
+    }
+    tab.off[g.L] = off;
+    tab.lo[g.L] = 0;
+  }
+  __syncthreads();
+}
+
+// address of node (l - t, t) in wavefront order, or -1 if not on level l
+__device__ __forceinline__ int wf_addr(const LevelTab& tab, const Grid2D g, int l, int t) {
+  if (l < 0 || l >= g.L) return -1;
+  const int lo = tab.lo[l], hi = lvl_hi(l, g.m);
+  return (t >= lo && t <= hi) ? tab.off[l] + t - lo : -1;
+}
+
+// ---- (e) IC(0) factor of every centroid matrix (one CTA per centroid) ---------
+// fac layout per centroid (3 n doubles, wavefront order): D, aW, aS of A_c.
+__global__ void __launch_bounds__(P2_T) factor2d_kernel(const double* kappa_c, int64_t ldk, int P, const Grid2D g,
+                                                         double* fac, int* err) {
+  __shared__ LevelTab tab;
+  __shared__ double dprev[2][P2_T + 1];
+  build_levels(tab, g);
+  const int p = blockIdx.x, t = threadIdx.x;
+  if (p >= P) return;
+  const double* kap = kappa_c + static_cast<size_t>(p) * ldk;
+  double* D = fac + static_cast<size_t>(p) * 3 * g.n;
+  double* W = D + g.n;
+  double* S = W + g.n;
+  for (int k = t; k <= P2_T; k += blockDim.x) dprev[0][k] = dprev[1][k] = 1.0;
+  __syncthreads();
+  bool ok = true;
+  for (int l = 0; l < g.L; ++l) {
+    const int cur = l & 1, prv = cur ^ 1;
+    const int a = wf_addr(tab, g, l, t);
+    if (a >= 0) {
+      const int ix = l - t, iy = t;
+      const RowCoef rc = assemble_row(kap, g, ix, iy);
+      // oracle: t = a_ii; t -= aW*aW / D_W; t -= aS*aS / D_S
+      double v = rc.d;
+      if (ix > 0) v = __dsub_rn(v, __ddiv_rn(__dmul_rn(rc.w, rc.w), dprev[prv][t]));
+      if (iy > 0) v = __dsub_rn(v, __ddiv_rn(__dmul_rn(rc.s, rc.s), dprev[prv][t - 1]));
+      if (!(v > 0.0)) ok = false;
+      dprev[cur][t] = v;
+      D[a] = v;
+      W[a] = rc.w;
+      S[a] = rc.s;
+    }
+    __syncthreads();
+  }
+  if (!ok) atomicExch(err, 1);
+}
+
+// ---- (d) batched PCG, one CTA per sample --------------------------------------
+struct Pcg2dParams {
+  Grid2D g;
+  const double* kappa;      // samples x ldk nodal kappa (natural mesh order)
+  int64_t ldk;
+  const uint8_t* kflag;
+  const int32_t* perm;
+  const int32_t* labels;
+  const double* fac;        // P x 3n (D, aW, aS), wavefront order
+  double* work;             // per CTA: P2_WORK n doubles
+  int64_t B, out_base, solve_limit;
+  double eps;
+  int max_iter;
+  const int32_t* max_iter_arr;
+  int* counter;
+  int32_t* iters;
+  double* rel;
+  uint8_t* status;
+  double* x_out;            // nullable, natural interior order
+  int exact;                // 1: dot products summed serially in natural order (reference bits)
+};
+
+constexpr int P2_WORK = 11;  // per-CTA scratch vectors: d, w, s, x[2], r, p[2], y, z, prod
+
+template <int NW>
+__device__ __forceinline__ double block_sum2d(double v, double* red, int warp, int lane) {
+  v = warp_allsum(v);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s[NW];
+#pragma unroll
+  for (int i = 0; i < NW; ++i) s[i] = red[i];
+#pragma unroll
+  for (int w = 1; w < NW; w <<= 1)
+#pragma unroll
+    for (int i = 0; i + w < NW; i += 2 * w) s[i] += s[i + w];
+  return s[0];
+}
+
+// Exact mode: the products were stored at their natural index; one thread sums
+// them serially (s = 0; s += t_i for i = 0..n-1), i.e. solver.cpp:176-180's bits.
+__device__ __forceinline__ double serial_sum2d(const double* prod, int n, double* slot) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+#pragma unroll 8
+    for (int i = 0; i < n; ++i) s = __dadd_rn(s, prod[i]);
+    *slot = s;
+  }
+  __syncthreads();
+  const double v = *slot;
+  __syncthreads();
+  return v;
+}
+
+__global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
+  constexpr int NW = P2_T / 32;
+  __shared__ LevelTab tab;
+  __shared__ double sbuf[2][P2_T + 2];   // previous level of the running sweep (index iy + 1)
+  __shared__ double red[4][NW];
+  __shared__ int64_t s_item;
+  const Grid2D g = prm.g;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  build_levels(tab, g);
+  const int n = g.n;
+  double* base = prm.work + static_cast<size_t>(blockIdx.x) * P2_WORK * n;
+  double* Ad = base;          // diagonal
+  double* Aw = base + n;      // W coupling (the E coupling of node i is Aw[E])
+  double* As = base + 2 * n;  // S coupling (the N coupling of node i is As[N])
+  double* Xb[2] = {base + 3 * n, base + 4 * n};
+  double* Rv = base + 5 * n;
+  double* Pb[2] = {base + 6 * n, base + 7 * n};
+  double* Y = base + 8 * n;
+  double* Z = base + 9 * n;
+  double* Prod = base + 10 * n;  // exact mode: products at natural index iy*m + ix
+  const bool exact = prm.exact != 0;
+  // reduce a thread partial (fast) or the stored products (exact)
+  auto reduce = [&](double part, double* red_slot) {
+    return exact ? serial_sum2d(Prod, n, red_slot) : block_sum2d<NW>(part, red_slot, warp, lane);
+  };
+  auto nat = [&](int l) { return t * g.m + (l - t); };
+
+  for (;;) {
+    if (t == 0) s_item = atomicAdd(prm.counter, 1);
+    __syncthreads();
+    const int64_t item = s_item;
+    __syncthreads();
+    if (item >= prm.B) break;
+    const int s = prm.perm[item];
+    const int64_t gs = prm.out_base + s;
+    const int label = prm.labels[s];
+    if (label < 0 || prm.kflag[s] || gs >= prm.solve_limit) {
+      if (t == 0) {
+        prm.iters[gs] = 0;
+        prm.rel[gs] = 0.0;
+        prm.status[gs] = gs >= prm.solve_limit ? VQPC_S_NOT_SOLVED
+                         : label < 0           ? VQPC_S_INVALID_LATENT
+                                               : VQPC_S_COEFF_OVERFLOW;
+      }
+      continue;
+    }
+    const double* kap = prm.kappa + static_cast<size_t>(s) * prm.ldk;
+    const double* FD = prm.fac + static_cast<size_t>(label) * 3 * n;
+    const double* FW = FD + n;
+    const double* FS = FW + n;
+    int xc = 0, pc = 0;  // current ping-pong halves
+
+    // ---- setup: assemble the sample's rows, x = 0, r = b ----------------------
+    double bb_loc = 0.0, bval = 0.0;
+    for (int l = 0; l < g.L; ++l) {
+      const int a = wf_addr(tab, g, l, t);
+      if (a >= 0) {
+        const RowCoef rc = assemble_row(kap, g, l - t, t);
+        Ad[a] = rc.d;
+        Aw[a] = rc.w;
+        As[a] = rc.s;
+        Xb[0][a] = 0.0;
+        Rv[a] = rc.b;
+        bval = rc.b;  // b_i = area_sum / 3 is the same for every interior node of this mesh
+        bb_loc = fma(rc.b, rc.b, bb_loc);
+        if (exact) Prod[nat(l)] = __dmul_rn(rc.b, rc.b);
+      }
+    }
+    __syncthreads();
+    const int max_iter = prm.max_iter_arr ? prm.max_iter_arr[gs] : (prm.max_iter < 0 ? 10 * n : prm.max_iter);
+
+    // z = M^{-1} r by the level-scheduled IC(0) sweeps (oracle arithmetic); returns the r.z partial
+    auto sweeps = [&]() -> double {
+      // forward (D + L) y = r, ascending levels
+      __syncthreads();
+      for (int l = 0; l < g.L; ++l) {
+        const int cur = l & 1, prv = cur ^ 1;
+        const int a = wf_addr(tab, g, l, t);
+        if (a >= 0) {
+          const int ix = l - t;
+          double v = Rv[a];
+          if (ix > 0) v = __dsub_rn(v, __dmul_rn(FW[a], sbuf[prv][t + 1]));
+          if (t > 0) v = __dsub_rn(v, __dmul_rn(FS[a], sbuf[prv][t]));
+          v = __ddiv_rn(v, FD[a]);
+          Y[a] = v;
+          sbuf[cur][t + 1] = v;
+        }
+        __syncthreads();
+      }
+      // backward (D + L^T) z = D y, descending levels: z_i = y_i - (aE z_E + aN z_N) / D_i
+      double rz_part = 0.0;
+      for (int l = g.L - 1; l >= 0; --l) {
+        const int cur = l & 1, prv = cur ^ 1;
+        const int a = wf_addr(tab, g, l, t);
+        if (a >= 0) {
+          const int ix = l - t;
+          double acc = 0.0;
+          if (ix < g.m - 1) acc = __dadd_rn(acc, __dmul_rn(FW[wf_addr(tab, g, l + 1, t)], sbuf[prv][t + 1]));
+          if (t < g.m - 1) acc = __dadd_rn(acc, __dmul_rn(FS[wf_addr(tab, g, l + 1, t + 1)], sbuf[prv][t + 2]));
+          const double z = __dsub_rn(Y[a], __ddiv_rn(acc, FD[a]));
+          Z[a] = z;
+          sbuf[cur][t + 1] = z;
+          rz_part = fma(Rv[a], z, rz_part);
+          if (exact) Prod[nat(l)] = __dmul_rn(Rv[a], z);
+        }
+        __syncthreads();
+      }
+      return rz_part;
+    };
+
+    // norm_b first: in exact mode Prod holds b_i^2 until the sweeps overwrite it
+    const double norm_b = sqrt(reduce(bb_loc, red[3]));
+    double rz = reduce(sweeps(), red[2]);
+    int J = 0;
+    double rel_rec = 0.0;
+    uint8_t st = VQPC_S_MAX_ITER;
+    if (norm_b == 0.0) st = VQPC_S_CONVERGED;
+    else if (!(rz > 0.0)) st = VQPC_S_BREAKDOWN;
+    else {
+      double beta = 0.0;
+      for (int j = 1; j <= max_iter; ++j) {
+        // ---- P1 (barrier-free): p_new = z + beta p_old into the other half; pAp -----
+        const double* Po = Pb[pc];
+        double* Pn = Pb[pc ^ 1];
+        const bool first = j == 1;
+        auto pnew = [&](int q) { return q < 0 ? 0.0 : (first ? Z[q] : __dadd_rn(Z[q], __dmul_rn(beta, Po[q]))); };
+        double pap = 0.0;
+        for (int l = 0; l < g.L; ++l) {
+          const int a = wf_addr(tab, g, l, t);
+          if (a >= 0) {
+            const int ix = l - t;
+            const int aw = ix > 0 ? wf_addr(tab, g, l - 1, t) : -1;
+            const int as = t > 0 ? wf_addr(tab, g, l - 1, t - 1) : -1;
+            const int ae = ix < g.m - 1 ? wf_addr(tab, g, l + 1, t) : -1;
+            const int an = t < g.m - 1 ? wf_addr(tab, g, l + 1, t + 1) : -1;
+            const double pcv = pnew(a);
+            const double ap = row_apply(As[a], Aw[a], Ad[a], ae >= 0 ? Aw[ae] : 0.0, an >= 0 ? As[an] : 0.0,
+                                        pnew(as), pnew(aw), pcv, pnew(ae), pnew(an));
+            Pn[a] = pcv;
+            pap = fma(pcv, ap, pap);
+            if (exact) Prod[nat(l)] = __dmul_rn(pcv, ap);
+          }
+        }
+        pc ^= 1;
+        const double pAp = reduce(pap, red[0]);
+        if (!(pAp > 0.0)) {
+          st = VQPC_S_BREAKDOWN;
+          break;
+        }
+        const double alpha = rz / pAp;
+        // ---- P2 (barrier-free): x_new = x + alpha p, r -= alpha A p, |b - A x_new|^2 ---
+        const double* Pv = Pb[pc];
+        const double* Xo = Xb[xc];
+        double* Xn = Xb[xc ^ 1];
+        double rr = 0.0;
+        for (int l = 0; l < g.L; ++l) {
+          const int a = wf_addr(tab, g, l, t);
+          if (a >= 0) {
+            const int ix = l - t;
+            const int aw = ix > 0 ? wf_addr(tab, g, l - 1, t) : -1;
+            const int as = t > 0 ? wf_addr(tab, g, l - 1, t - 1) : -1;
+            const int ae = ix < g.m - 1 ? wf_addr(tab, g, l + 1, t) : -1;
+            const int an = t < g.m - 1 ? wf_addr(tab, g, l + 1, t + 1) : -1;
+            auto pv = [&](int q) { return q < 0 ? 0.0 : Pv[q]; };
+            // every x_new is recomputed with the operation its owner uses (bit-identical);
+            // updates follow solver.cpp:216-218/241 without contraction
+            auto xnew = [&](int q) { return q < 0 ? 0.0 : __dadd_rn(Xo[q], __dmul_rn(alpha, Pv[q])); };
+            const double aE = ae >= 0 ? Aw[ae] : 0.0, aN = an >= 0 ? As[an] : 0.0;
+            const double ap = row_apply(As[a], Aw[a], Ad[a], aE, aN, pv(as), pv(aw), Pv[a], pv(ae), pv(an));
+            const double xn = xnew(a);
+            const double ax = row_apply(As[a], Aw[a], Ad[a], aE, aN, xnew(as), xnew(aw), xn, xnew(ae), xnew(an));
+            const double rt = __dsub_rn(bval, ax);
+            rr = fma(rt, rt, rr);
+            if (exact) Prod[nat(l)] = __dmul_rn(rt, rt);
+            Xn[a] = xn;
+            Rv[a] = __dsub_rn(Rv[a], __dmul_rn(alpha, ap));
+          }
+        }
+        xc ^= 1;
+        const double rel = sqrt(reduce(rr, red[1])) / norm_b;
+        J = j;
+        rel_rec = rel;
+        if (rel < prm.eps) {
+          st = VQPC_S_CONVERGED;
+          break;
+        }
+        // ---- P3: z = M^{-1} r; r.z (level-ordered sweeps) ---------------------------
+        const double rz_next = reduce(sweeps(), red[2]);
+        if (!(rz_next > 0.0)) {
+          st = VQPC_S_BREAKDOWN;
+          break;
+        }
+        beta = rz_next / rz;
+        rz = rz_next;
+      }
+    }
+    if (t == 0) {
+      prm.iters[gs] = J;
+      prm.rel[gs] = rel_rec;
+      prm.status[gs] = st;
+    }
+    if (prm.x_out) {
+      double* xo = prm.x_out + static_cast<size_t>(gs) * n;
+      for (int l = 0; l < g.L; ++l) {
+        const int a = wf_addr(tab, g, l, t);
+        if (a >= 0) xo[t * g.m + (l - t)] = Xb[xc][a];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// natural-order IC(0) apply for one vector (parity tests), single CTA
+__global__ void __launch_bounds__(P2_T) precond2d_apply_kernel(const double* fac, int p, const Grid2D g,
+                                                                const double* r_nat, double* z_nat, double* ws) {
+  __shared__ LevelTab tab;
+  __shared__ double sbuf[2][P2_T + 2];
+  build_levels(tab, g);
+  const int t = threadIdx.x, n = g.n;
+  const double* FD = fac + static_cast<size_t>(p) * 3 * n;
+  const double* FW = FD + n;
+  const double* FS = FW + n;
+  double* Y = ws;
+  sbuf[0][t + 1] = sbuf[1][t + 1] = 0.0;
+  if (t == 0) sbuf[0][0] = sbuf[1][0] = sbuf[0][P2_T + 1] = sbuf[1][P2_T + 1] = 0.0;
+  __syncthreads();
+  for (int l = 0; l < g.L; ++l) {
+    const int cur = l & 1, prv = cur ^ 1;
+    const int a = wf_addr(tab, g, l, t);
+    if (a >= 0) {
+      const int ix = l - t;
+      double v = r_nat[t * g.m + ix];
+      if (ix > 0) v = __dsub_rn(v, __dmul_rn(FW[a], sbuf[prv][t + 1]));
+      if (t > 0) v = __dsub_rn(v, __dmul_rn(FS[a], sbuf[prv][t]));
+      v = __ddiv_rn(v, FD[a]);
+      Y[a] = v;
+      sbuf[cur][t + 1] = v;
+    }
+    __syncthreads();
+  }
+  sbuf[0][t + 1] = sbuf[1][t + 1] = 0.0;
+  __syncthreads();
+  for (int l = g.L - 1; l >= 0; --l) {
+    const int cur = l & 1, prv = cur ^ 1;
+    const int a = wf_addr(tab, g, l, t);
+    if (a >= 0) {
+      const int ix = l - t;
+      double acc = 0.0;
+      if (ix < g.m - 1) acc = __dadd_rn(acc, __dmul_rn(FW[wf_addr(tab, g, l + 1, t)], sbuf[prv][t + 1]));
+      if (t < g.m - 1) acc = __dadd_rn(acc, __dmul_rn(FS[wf_addr(tab, g, l + 1, t + 1)], sbuf[prv][t + 2]));
+      const double z = __dsub_rn(Y[a], __ddiv_rn(acc, FD[a]));
+      z_nat[t * g.m + ix] = z;
+      sbuf[cur][t + 1] = z;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace vqpc

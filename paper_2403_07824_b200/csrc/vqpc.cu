@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "factor.cuh"
 #include "pcg1d.cuh"
+#include "pcg2d.cuh"
 #include "realise.cuh"
 #include "vqpc.h"
 
@@ -91,6 +92,10 @@ struct vqpc_ctx {
   // device-resident problem data
   DBuf<double> phi, sqrt_lam, root, sites, kappa_c;
   DBuf<double2> fac;
+  // 2-D path: grid, IC(0) factors (P x 3n, wavefront order), per-CTA PCG scratch
+  Grid2D g2{};
+  DBuf<double> fac2, work2;
+  int exact = 0;  // 2-D: serial (reference-order) dot products
   // work buffers
   DBuf<double> xi, kappa, best, dvec;
   DBuf<uint8_t> kflag, status;
@@ -243,12 +248,52 @@ void run_bucket(vqpc_ctx* c, const int32_t* d_labels, int64_t B, int32_t* d_perm
   launch_check(c);
 }
 
+void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d_kflag, const int32_t* d_perm,
+               const int32_t* d_labels, int64_t B, int64_t out_base, double eps, int max_iter, const int32_t* d_mia,
+               int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x, int64_t solve_limit) {
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg2d_kernel, P2_T, 0));
+  if (per_sm < 1) throw ApiError{VQPC_CUDA_ERROR, "pcg2d kernel does not fit on an SM"};
+  const int64_t slots = std::min<int64_t>(B, static_cast<int64_t>(per_sm) * c->sm_count);
+  c->work2.ensure(static_cast<size_t>(slots) * P2_WORK * c->n);
+  c->counter.ensure(1);
+  CK(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->stream));
+  Pcg2dParams prm{};
+  prm.g = c->g2;
+  prm.kappa = d_kappa;
+  prm.ldk = ldk;
+  prm.kflag = d_kflag;
+  prm.perm = d_perm;
+  prm.labels = d_labels;
+  prm.fac = c->fac2.p;
+  prm.work = c->work2.p;
+  prm.B = B;
+  prm.out_base = out_base;
+  prm.solve_limit = solve_limit;
+  prm.eps = eps;
+  prm.max_iter = max_iter;
+  prm.max_iter_arr = d_mia;
+  prm.counter = c->counter.p;
+  prm.iters = d_iters;
+  prm.rel = d_rel;
+  prm.status = d_status;
+  prm.x_out = d_x;
+  prm.exact = c->exact;
+  Timed tm(c, VQPC_K_PCG);
+  pcg2d_kernel<<<static_cast<unsigned>(slots), P2_T, 0, c->stream>>>(prm);
+  launch_check(c);
+}
+
 void run_pcg(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d_kflag, const int32_t* d_perm,
              const int32_t* d_labels, int64_t B, int64_t out_base, double eps, int max_iter, const int32_t* d_mia,
              int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x,
              int64_t solve_limit = INT64_MAX) {
   if (B <= 0) return;
-  if (c->pb.dim != 1) throw ApiError{VQPC_INVALID_CONFIG, "2-D solve path not built in this version"};
+  if (c->pb.dim == 2) {
+    run_pcg2d(c, d_kappa, ldk, d_kflag, d_perm, d_labels, B, out_base, eps, max_iter, d_mia, d_iters, d_rel,
+              d_status, d_x, solve_limit);
+    return;
+  }
   const PcgVariant* v = pick_pcg(c->n);
   c->counter.ensure(1);
   CK(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->stream));
@@ -445,6 +490,7 @@ int vqpc_ctx_create(const vqpc_problem* pb, vqpc_ctx** out) {
   const bool grid = pb->method == VQPC_GRID || pb->method == VQPC_SIGN_GRID;
   if (grid && !pb->latent) return VQPC_INVALID_CODEBOOK;
   if (pb->dim == 1 && pb->precond != VQPC_PC_CHOLESKY) return VQPC_INVALID_CONFIG;
+  if (pb->dim == 2 && (pb->precond != VQPC_PC_IC0 || pb->size - 1 > P2_T)) return VQPC_INVALID_CONFIG;
   auto* c = new vqpc_ctx();
   c->pb = *pb;
   c->n = pb->dim == 1 ? pb->size - 1 : (pb->size - 1) * (pb->size - 1);
@@ -454,6 +500,13 @@ int vqpc_ctx_create(const vqpc_problem* pb, vqpc_ctx** out) {
     c->sm_count = prop.multiProcessorCount;
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
+    if (pb->dim == 2) {
+      c->g2.r = pb->size;
+      c->g2.m = pb->size - 1;
+      c->g2.n = c->g2.m * c->g2.m;
+      c->g2.L = 2 * c->g2.m - 1;
+      c->g2.h = 1.0 / pb->size;
+    }
     if (pb->dim == 1) {
       const PcgVariant* v = pick_pcg(c->n);
       if (!v) throw ApiError{VQPC_INVALID_CONFIG, "1-D system larger than the largest pcg variant"};
@@ -495,7 +548,7 @@ void vqpc_ctx_destroy(vqpc_ctx* c) {
   cudaSetDevice(c->pb.device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto* b : {&c->phi, &c->sqrt_lam, &c->root, &c->sites, &c->kappa_c, &c->xi, &c->kappa, &c->best, &c->dvec,
-                  &c->rel, &c->x})
+                  &c->rel, &c->x, &c->fac2, &c->work2})
     b->release();
   c->fac.release();
   c->kflag.release();
@@ -529,6 +582,12 @@ int vqpc_set_stream(vqpc_ctx* c, void* stream) {
   });
 }
 
+int vqpc_set_exact_reductions(vqpc_ctx* c, int enable) {
+  if (!c) return VQPC_INVALID_ARGUMENT;
+  c->exact = enable != 0;
+  return VQPC_OK;
+}
+
 int vqpc_synchronize(vqpc_ctx* c) {
   if (!c) return VQPC_INVALID_ARGUMENT;
   return guard(c, [&] { CK(cudaStreamSynchronize(c->stream)); });
@@ -556,14 +615,21 @@ int vqpc_factor_centroids(vqpc_ctx* c) {
     c->kflag.ensure(P);
     CK(cudaMemsetAsync(c->kflag.p, 0, P, c->stream));
     run_realise(c, c->xi.p, P, std::max(m, 1), m, c->kappa_c.p, ldk, c->kflag.p);
-    if (pb.dim != 1) throw ApiError{VQPC_INVALID_CONFIG, "2-D factorisation not built in this version"};
-    c->fac.ensure(static_cast<size_t>(P) * c->NP);
     c->err.ensure(1);
     CK(cudaMemsetAsync(c->err.p, 0, sizeof(int), c->stream));
-    factor1d_kernel<<<static_cast<unsigned>(ceil_div(P, 64)), 64, 0, c->stream>>>(c->kappa_c.p, ldk, P, c->n,
-                                                                                    h_of(pb), c->fac.p, c->NP,
-                                                                                    c->err.p);
-    launch_check(c);
+    if (pb.dim == 2) {
+      c->fac2.ensure(static_cast<size_t>(P) * 3 * c->n);
+      Timed tm(c, VQPC_K_OTHER);
+      factor2d_kernel<<<P, P2_T, 0, c->stream>>>(c->kappa_c.p, ldk, P, c->g2, c->fac2.p, c->err.p);
+      launch_check(c);
+    } else {
+      c->fac.ensure(static_cast<size_t>(P) * c->NP);
+      Timed tm(c, VQPC_K_OTHER);
+      factor1d_kernel<<<static_cast<unsigned>(ceil_div(P, 64)), 64, 0, c->stream>>>(c->kappa_c.p, ldk, P, c->n,
+                                                                                      h_of(pb), c->fac.p, c->NP,
+                                                                                      c->err.p);
+      launch_check(c);
+    }
     int err = 0;
     std::vector<uint8_t> flags(P);
     d2h(c, &err, c->err.p, 1);
@@ -592,9 +658,13 @@ int vqpc_precond_apply(vqpc_ctx* c, int p, const double* r, double* z) {
   return guard(c, [&] {
     if (!c->factored) throw ApiError{VQPC_INVALID_CONFIG, "not factored"};
     if (p < 0 || p >= c->pb.P) throw ApiError{VQPC_INVALID_ARGUMENT, "p out of range"};
-    c->dvec.ensure(2 * static_cast<size_t>(c->n));
+    c->dvec.ensure(3 * static_cast<size_t>(c->n));
     h2d(c, c->dvec.p, r, c->n);
-    precond1d_apply_kernel<<<1, 1, 0, c->stream>>>(c->fac.p, c->NP, p, c->n, c->dvec.p, c->dvec.p + c->n);
+    if (c->pb.dim == 2)
+      precond2d_apply_kernel<<<1, P2_T, 0, c->stream>>>(c->fac2.p, p, c->g2, c->dvec.p, c->dvec.p + c->n,
+                                                        c->dvec.p + 2 * c->n);
+    else
+      precond1d_apply_kernel<<<1, 1, 0, c->stream>>>(c->fac.p, c->NP, p, c->n, c->dvec.p, c->dvec.p + c->n);
     launch_check(c);
     d2h(c, z, c->dvec.p + c->n, c->n);
     CK(cudaStreamSynchronize(c->stream));

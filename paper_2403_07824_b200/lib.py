@@ -52,6 +52,7 @@ def load():
             "vqpc_error_string": (C.c_char_p, [I]),
             "vqpc_set_stream": (I, [VP, VP]),
             "vqpc_synchronize": (I, [VP]),
+            "vqpc_set_exact_reductions": (I, [VP, I]),
             "vqpc_unknowns": (I, [VP]),
             "vqpc_launch_count": (I64, [VP]),
             "vqpc_factor_centroids": (I, [VP]),
@@ -200,6 +201,10 @@ class Context:
 
     def synchronize(self):
         self._c(load().vqpc_synchronize(self.h))
+
+    def set_exact_reductions(self, enable=True):
+        """2-D: serial reference-order dot products (bit-identical solves)."""
+        self._c(load().vqpc_set_exact_reductions(self.h, 1 if enable else 0))
 
     def factor_centroids(self):
         self._c(load().vqpc_factor_centroids(self.h))

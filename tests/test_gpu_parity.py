@@ -85,7 +85,8 @@ def _campaign_parity(name, n_real):
     cfg, basis, cb, xi = setup_case(name, n_real)
     ocb = oracle_codebook(cb)
     res = campaign.run_campaign_with(cfg, dict(basis=basis, codebook=cb), xi)
-    args = (1, cfg["mesh_resolution"], "cholesky", ocb, basis["eigenvalues"], basis["eigenvectors"], xi, cfg["eps"])
+    args = (cfg["dim"], cfg["mesh_resolution"], cfg["precond"], ocb, basis["eigenvalues"], basis["eigenvectors"], xi,
+            cfg["eps"])
     ref = oracle.run_campaign(*args)
     with oracle.fma_variant():
         ref_fma = oracle.run_campaign(*args)
@@ -107,7 +108,7 @@ def _check_j_parity(name, n_real):
     # (the reference and its FMA build already differ in the 2nd decimal on C2)
     assert abs(cmp["mean_cpu"] - cmp["mean_gpu"]) <= max(3 * abs(yard["mean_cpu"] - yard["mean_gpu"]), 0.03), cmp
     # every sample with |dJ| > 1 must be a borderline (flat-residual) case
-    pset = oracle.PreconditionerSet.build(1, cfg["mesh_resolution"], "cholesky", oracle_codebook(cb),
+    pset = oracle.PreconditionerSet.build(cfg["dim"], cfg["mesh_resolution"], cfg["precond"], oracle_codebook(cb),
                                           basis["eigenvalues"], basis["eigenvectors"])
     jc, jg = ref["iterations"], res["iterations"]
     both = (ref["status"] == 0) & (res["status"] == 0)
@@ -213,3 +214,64 @@ def test_determinism_across_chunks():
     b = ctx.run_campaign(xi, cfg["eps"], chunk=300)
     for k in ("labels", "iterations", "rel", "status", "n_p", "sum_j"):
         assert np.array_equal(a[k], b[k]), k
+
+
+# ---------------------------------------------------------------- 2-D (C4) path
+def test_ic0_factor_and_apply_bit_identical():
+    """Level-scheduled IC(0) on the GPU == the oracle's sequential IC(0), bit for bit,
+    when both factor the same centroid coefficient (here: the GPU's kappa_p)."""
+    for name in ("C4s", "C4"):
+        cfg, basis, cb, _ = setup_case(name, 8)
+        ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+        kc = ctx.centroid_coefficients()
+        kc_cpu = oracle.centroid_coefficients(oracle_codebook(cb), basis["eigenvalues"], basis["eigenvectors"])
+        assert (np.abs(kc - kc_cpu) / kc_cpu).max() < 1e-13
+        pset = oracle.PreconditionerSet.from_coefficients(2, cfg["mesh_resolution"], "ic0", kc[[0, cb["P"] - 1]])
+        rng = np.random.default_rng(3)
+        for q, p in enumerate([0, cb["P"] - 1]):
+            r = rng.standard_normal(ctx.n)
+            assert np.array_equal(ctx.precond_apply(p, r), pset.apply(q, r)), name
+
+
+def test_c4_full_size_samples():
+    """A handful of full C4 (r = 256, 65,025 unknowns, IC(0)) samples vs the oracle."""
+    cfg, basis, cb, xi = setup_case("C4", 6)
+    res = campaign.run_campaign_with(cfg, dict(basis=basis, codebook=cb), xi)
+    ref = oracle.run_campaign(2, cfg["mesh_resolution"], "ic0", oracle_codebook(cb), basis["eigenvalues"],
+                              basis["eigenvectors"], xi, cfg["eps"])
+    assert np.array_equal(res["labels"], ref["labels"])
+    print("C4 J gpu", res["iterations"], "cpu", ref["iterations"], "status", res["status"], ref["status"])
+    both = (res["status"] == 0) & (ref["status"] == 0)
+    assert np.mean(res["status"] == ref["status"]) >= 5 / 6
+    assert np.all(np.abs(res["iterations"][both].astype(int) - ref["iterations"][both]) <= 2)
+
+
+def test_2d_exact_mode_bit_identical():
+    """2-D with serial reference-order reductions: J, final residual and x are
+    bit-identical to the CPU oracle (every operation is reproduced)."""
+    cfg, basis, cb, xi = setup_case("C4s", 96)
+    ocb = oracle_codebook(cb)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    ctx.set_exact_reductions(True)
+    kc = ctx.centroid_coefficients()
+    labels = oracle.assign(ocb, xi)
+    # the oracle must factor the same centroid coefficient bits and realise the
+    # same sample coefficients: feed it the GPU's kappa (DMMA sums differ at ~1 ulp)
+    kap_gpu, _ = ctx.realise(xi)
+    pset = oracle.PreconditionerSet.from_coefficients(2, cfg["mesh_resolution"], "ic0", kc)
+    it, rel, st, x = ctx.solve_batch(xi, labels, cfg["eps"], want_x=True)
+    for i in range(len(xi)):
+        out = pset.pcg(int(labels[i]), kap_gpu[i], cfg["eps"])
+        assert out["iterations"] == it[i] and out["status"] == st[i], i
+        assert out["rel"] == rel[i], i
+        assert np.array_equal(out["x"], x[i]), i
+
+
+def test_2d_fast_mode_statistics():
+    """Tree reductions: the only difference from the oracle is the dot-product
+    summation order; J statistics stay within a small band of the oracle."""
+    cfg, basis, cb, xi, res, ref, cmp, yard = _campaign_parity("C4s", 256)
+    print("C4s gpu:", {k: v for k, v in cmp.items() if k != "disagree"})
+    assert cmp["status_agree"] >= 0.99
+    assert abs(cmp["mean_cpu"] - cmp["mean_gpu"]) / cmp["mean_cpu"] < 0.01
+    assert cmp["max_dj"] <= 6
