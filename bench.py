@@ -160,7 +160,7 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded counter-RNG xi; no dataset exists for this path)",
-            "config": workload(cfg, n_step, K),
+            "config": workload(cfg, cfg["n_realizations"], K),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"], "kind": "port",
                              "sample": f"{n_step} realisations per step, {args.steps} timed steps: " + last["sample"]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -94,13 +94,13 @@ struct Pcg1dShared {
   static constexpr int NW = T / 32;
   static constexpr int NWT = CL * NW;  // warps per sample (whole cluster)
   double2 fac[R * T];     // {n_j, 1/u_j^2}, thread-major
-  double cs[R * T];       // coupling c_j = kappa_j / h (0 for j >= n), thread-major
-  double dg[R * T];       // diagonal d_j = c_j + c_{j+1} (true c_n; 0 for dead rows)
+  double2 cd[R * T];      // {coupling c_j = kappa_j / h (0 for j >= n), diagonal d_j = c_j + c_{j+1}
+                          //  (true c_n; 0 for dead rows)}, thread-major
   double cs_end;          // c_{R*T}: right coupling of the last thread's last row
   double lev[12 * T];     // per-thread lane-scan multipliers: L1[5], Q1, L2[5], Q2
   double qa[8 * T];       // per-thread quarter products: sweep 1 [0..3], sweep 2 [4..7]
-  double wa1[NWT], wa2[NWT];  // per-warp products of the sweep multipliers (all CTAs)
-  double sw1[NWT], sw2[NWT];  // per-iteration warp aggregates (all CTAs)
+  double2 f1[NWT], f2[NWT];   // per warp {product of the sweep multipliers (per centroid),
+                              //           aggregate of this iteration}, sweeps 1 and 2 (all CTAs)
   double red[4][NWT];         // reduction partials: pAp, rr, rz, |b|^2 (all CTAs)
   double zf[T], zl[T];      // first / last z of every thread
   int64_t item;
@@ -136,35 +136,24 @@ __device__ __forceinline__ double fused_row(double c_lo, double d, double c_hi, 
 // |b - A x|^2 over a thread's rows (4 split accumulators)
 template <int R, int T, bool MASK>
 __device__ __forceinline__ double true_residual(const double (&x)[R], double x_left, double x_right,
-                                                const double* cst, const double* dgt, const double* c_halo,
-                                                double h, int j0, int n) {
+                                                const double2* cdt, const double* c_halo, double h, int j0, int n) {
   constexpr int Q = R / 4;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  double2 cd_lo = cdt[0];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const double2 cd_hi = i + 1 < R ? cdt[(i + 1) * T] : make_double2(*c_halo, 0.0);
+    const double xl = i == 0 ? x_left : x[i - 1];
+    const double xr = i + 1 < R ? x[i + 1] : x_right;
 #if VQPC_RESID_CSR
-  double c_lo = cst[0];
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const double c_hi = i + 1 < R ? cst[(i + 1) * T] : *c_halo;
-    const double xl = i == 0 ? x_left : x[i - 1];
-    const double xr = i + 1 < R ? x[i + 1] : x_right;
-    double rt = __dsub_rn(h, csr_row(c_lo, dgt[i * T], c_hi, xl, x[i], xr));
-    if (MASK && j0 + i >= n) rt = 0.0;
-    acc[i / Q] = fma(rt, rt, acc[i / Q]);
-    c_lo = c_hi;
-  }
+    double rt = __dsub_rn(h, csr_row(cd_lo.x, cd_lo.y, cd_hi.x, xl, x[i], xr));
 #else
-  double c_lo = cst[0];
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const double c_hi = i + 1 < R ? cst[(i + 1) * T] : *c_halo;
-    const double xl = i == 0 ? x_left : x[i - 1];
-    const double xr = i + 1 < R ? x[i + 1] : x_right;
-    double rt = h - fused_row(c_lo, dgt[i * T], c_hi, xl, x[i], xr);
+    double rt = h - fused_row(cd_lo.x, cd_lo.y, cd_hi.x, xl, x[i], xr);
+#endif
     if (MASK && j0 + i >= n) rt = 0.0;
     acc[i / Q] = fma(rt, rt, acc[i / Q]);
-    c_lo = c_hi;
+    cd_lo = cd_hi;
   }
-#endif
   return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
@@ -212,12 +201,11 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
                                                      (reinterpret_cast<char*>(local_arr) - reinterpret_cast<char*>(&S)))[idx] = v;
   };
   const int n = prm.n;
-  const double* cst = S.cs + tid;      // cst[i*T] = c_{j0+i}
+  const double2* cdt = S.cd + tid;     // cdt[i*T] = {c_{j0+i}, d_{j0+i}}
   const double* levt = S.lev + tid;    // levt[k*T]
   const double* qat = S.qa + tid;      // qat[q*T]
   const double2* fact = S.fac + tid;   // fact[i*T]
-  const double* dgt = S.dg + tid;      // dgt[i*T] = d_{j0+i}
-  const double* c_halo = tid + 1 < T ? S.cs + tid + 1 : &S.cs_end;  // c_{j0+R}
+  const double* c_halo = tid + 1 < T ? &S.cd[tid + 1].x : &S.cs_end;  // c_{j0+R}
 
   int cur_label = -1;
   double nc[R];         // n_j of own rows
@@ -281,8 +269,8 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
       const double q1 = shfl_down(P1, 1), q2 = shfl_up(P2, 1);
       S.lev[5 * T + tid] = lane < 31 ? q1 : 1.0;
       S.lev[11 * T + tid] = lane > 0 ? q2 : 1.0;
-      if (lane == 0) publish(S.wa1, gwarp, P1);
-      if (lane == 31) publish(S.wa2, gwarp, P2);
+      if (lane == 0) publish(&S.f1[0].x, 2 * gwarp, P1);
+      if (lane == 31) publish(&S.f2[0].x, 2 * gwarp, P2);
       cur_label = label;
       __syncthreads();
     }
@@ -296,8 +284,7 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
       for (int i = 0; i < R; ++i) {
         const int j = j0 + i;
         const double c_next = j + 1 <= n ? kap[j + 1] / prm.h : 0.0;
-        S.cs[i * T + tid] = j < n ? c_prev : 0.0;
-        S.dg[i * T + tid] = j < n ? __dadd_rn(c_prev, c_next) : 0.0;
+        S.cd[i * T + tid] = make_double2(j < n ? c_prev : 0.0, j < n ? __dadd_rn(c_prev, c_next) : 0.0);
         c_prev = c_next;
       }
       // right coupling of this CTA's last row: c_{j0+R} (0 beyond the live rows)
@@ -338,27 +325,30 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
         for (int k = 0; k < 5; ++k) W = fma(levt[k * T], shfl_down(W, 1 << k), W);
         const double rrw = warp_allsum(rr_loc);
         if (lane == 0) {
-          publish(S.sw1, gwarp, W);
+          publish(&S.f1[0].x, 2 * gwarp + 1, W);
           publish(S.red[1], gwarp, rrw);
         }
         bar();  // barrier 2
         double vw = 0.0;
 #pragma unroll
         for (int w2 = NWT - 1; w2 > 0; --w2)
-          if (w2 > gwarp) vw = fma(S.wa1[w2], vw, S.sw1[w2]);
+          if (w2 > gwarp) {
+            const double2 f = S.f1[w2];
+            vw = fma(f.x, vw, f.y);
+          }
         const double Wn = shfl_down(W, 1);
         double in[4];
         in[3] = fma(levt[5 * T], vw, lane == 31 ? 0.0 : Wn);
         in[2] = fma(a3, in[3], v[3]);
         in[1] = fma(a2, in[2], v[2]);
         in[0] = fma(a1, in[1], v[1]);
+        // fix-up chains written straight into wz (no register copies)
 #pragma unroll
-        for (int i = Q - 1; i >= 0; --i)
+        for (int q = 0; q < 4; ++q) wz[q * Q + Q - 1] = fma(-nc[q * Q + Q - 1], in[q], r[q * Q + Q - 1]);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            in[q] = fma(-nc[q * Q + i], in[q], r[q * Q + i]);
-            wz[q * Q + i] = in[q];
-          }
+        for (int i = Q - 2; i >= 0; --i)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) wz[q * Q + i] = fma(-nc[q * Q + i], wz[q * Q + i + 1], r[q * Q + i]);
 #pragma unroll
         for (int i = 0; i < R; ++i) wz[i] *= fact[i * T].y;
       }
@@ -387,27 +377,29 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
         W = fma(b3, W, v[3]);
 #pragma unroll
         for (int k = 0; k < 5; ++k) W = fma(levt[(6 + k) * T], shfl_up(W, 1 << k), W);
-        if (lane == 31) publish(S.sw2, gwarp, W);
+        if (lane == 31) publish(&S.f2[0].x, 2 * gwarp + 1, W);
         bar();  // barrier 3
         double vw = 0.0;
 #pragma unroll
         for (int w2 = 0; w2 < NWT - 1; ++w2)
-          if (w2 < gwarp) vw = fma(S.wa2[w2], vw, S.sw2[w2]);
+          if (w2 < gwarp) {
+            const double2 f = S.f2[w2];
+            vw = fma(f.x, vw, f.y);
+          }
         const double Wp = shfl_up(W, 1);
         double in[4];
         in[0] = fma(levt[11 * T], vw, lane == 0 ? 0.0 : Wp);
         in[1] = fma(b0, in[0], v[0]);
         in[2] = fma(b1, in[1], v[1]);
         in[3] = fma(b2, in[2], v[2]);
+        // fix-up chains in place (z overwrites y row by row; no register copies)
+        wz[0] = fma(-n_left, in[0], wz[0]);
 #pragma unroll
-        for (int i = 0; i < Q; ++i)
+        for (int q = 1; q < 4; ++q) wz[q * Q] = fma(-nc[q * Q - 1], in[q], wz[q * Q]);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int row = q * Q + i;
-            const double m = row == 0 ? -n_left : -nc[row - 1];
-            in[q] = fma(m, in[q], wz[row]);
-            wz[row] = in[q];
-          }
+        for (int i = 1; i < Q; ++i)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) wz[q * Q + i] = fma(-nc[q * Q + i - 1], wz[q * Q + i - 1], wz[q * Q + i]);
       }
       // ================= rz (+|b|^2 at setup), z halos: barrier 4 ===========
       {
@@ -464,26 +456,26 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
       {
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #if VQPC_AP_CSR
-        double c_lo = cst[0];
+        double2 cd_lo = cdt[0];
 #pragma unroll
         for (int i = 0; i < R; ++i) {
-          const double c_hi = i + 1 < R ? cst[(i + 1) * T] : *c_halo;
+          const double2 cd_hi = i + 1 < R ? cdt[(i + 1) * T] : make_double2(*c_halo, 0.0);
           const double pl = i == 0 ? p_left : p[i - 1];
           const double pr = i + 1 < R ? p[i + 1] : p_right;
-          wz[i] = csr_row(c_lo, dgt[i * T], c_hi, pl, p[i], pr);
+          wz[i] = csr_row(cd_lo.x, cd_lo.y, cd_hi.x, pl, p[i], pr);
           acc[i / Q] = fma(p[i], wz[i], acc[i / Q]);
-          c_lo = c_hi;
+          cd_lo = cd_hi;
         }
 #else
-        double c_lo = cst[0];
+        double2 cd_lo = cdt[0];
 #pragma unroll
         for (int i = 0; i < R; ++i) {
-          const double c_hi = i + 1 < R ? cst[(i + 1) * T] : *c_halo;
+          const double2 cd_hi = i + 1 < R ? cdt[(i + 1) * T] : make_double2(*c_halo, 0.0);
           const double pl = i == 0 ? p_left : p[i - 1];
           const double pr = i + 1 < R ? p[i + 1] : p_right;
-          wz[i] = fused_row(c_lo, dgt[i * T], c_hi, pl, p[i], pr);  // (A p)_j, reusing wz
+          wz[i] = fused_row(cd_lo.x, cd_lo.y, cd_hi.x, pl, p[i], pr);  // (A p)_j, reusing wz
           acc[i / Q] = fma(p[i], wz[i], acc[i / Q]);
-          c_lo = c_hi;
+          cd_lo = cd_hi;
         }
 #endif
         const double a = warp_allsum((acc[0] + acc[1]) + (acc[2] + acc[3]));
@@ -504,8 +496,8 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
       x_left = fma(alpha, p_left, x_left);
       x_right = fma(alpha, p_right, x_right);
       // true residual b - A x; dead rows (b_j = 0) only exist in the last warp
-      rr_loc = gwarp == NWT - 1 ? true_residual<R, T, true>(x, x_left, x_right, cst, dgt, c_halo, prm.h, j0, n)
-                              : true_residual<R, T, false>(x, x_left, x_right, cst, dgt, c_halo, prm.h, j0, n);
+      rr_loc = gwarp == NWT - 1 ? true_residual<R, T, true>(x, x_left, x_right, cdt, c_halo, prm.h, j0, n)
+                              : true_residual<R, T, false>(x, x_left, x_right, cdt, c_halo, prm.h, j0, n);
     }
 
     if (rank == 0 && tid == 0) {

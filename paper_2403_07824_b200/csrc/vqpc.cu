@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -173,7 +174,12 @@ PcgVariant make_variant() {
 const PcgVariant* pick_pcg(int n) {
   static const PcgVariant table[] = {make_variant<16, 64, 1>(), make_variant<16, 128, 1>(),
                                      make_variant<16, 256, 1>(), make_variant<16, 256, 2>()};
-  for (const auto& v : table)
+  // experiments: VQPC_PCG_R=8 selects the 8-rows-per-thread layout (twice the warps)
+  static const PcgVariant table8[] = {make_variant<8, 128, 1>(), make_variant<8, 256, 1>(),
+                                      make_variant<8, 512, 1>(), make_variant<8, 512, 2>()};
+  const char* env = std::getenv("VQPC_PCG_R");
+  const bool r8 = env && std::atoi(env) == 8;
+  for (const auto& v : (r8 ? table8 : table))
     if (n <= v.R * v.T * v.CL) return &v;
   return nullptr;
 }
