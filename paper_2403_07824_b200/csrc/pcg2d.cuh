@@ -153,6 +153,8 @@ __device__ __forceinline__ double row_apply(double as, double aw, double d, doub
 struct LevelTab {
   int off[P2_MAXL + 2];  // level offsets (off[L] = n)
   int lo[P2_MAXL + 2];   // smallest iy of each level
+  int dw[P2_MAXL + 2];   // a - a_W for nodes of level l (a_S = a_W - 1)
+  int de[P2_MAXL + 2];   // a_E - a for nodes of level l (a_N = a_E + 1)
 };
 
 __device__ inline void build_levels(LevelTab& tab, const Grid2D g) {
@@ -165,6 +167,11 @@ __device__ inline void build_levels(LevelTab& tab, const Grid2D g) {
     }
     tab.off[g.L] = off;
     tab.lo[g.L] = 0;
+    for (int l = 0; l < g.L; ++l) {
+      const int size_l = tab.off[l + 1] - tab.off[l];
+      tab.dw[l] = l > 0 ? (tab.off[l] - tab.off[l - 1]) + tab.lo[l - 1] - tab.lo[l] : 0;
+      tab.de[l] = l + 1 < g.L ? size_l + tab.lo[l] - tab.lo[l + 1] : 0;
+    }
   }
   __syncthreads();
 }
@@ -233,9 +240,23 @@ struct Pcg2dParams {
   uint8_t* status;
   double* x_out;            // nullable, natural interior order
   int exact;                // 1: dot products summed serially in natural order (reference bits)
+  const int* gmap;          // per wavefront address: level | (iy << 16)
 };
 
 constexpr int P2_WORK = 11;  // per-CTA scratch vectors: d, w, s, x[2], r, p[2], y, z, prod
+constexpr int P2_DEPTH = 6;  // cp.async prefetch ring depth (levels) for the IC(0) sweeps
+constexpr int P2_NOPS = 5;   // operands per node in the ring
+constexpr size_t P2_DSMEM = sizeof(double) * P2_DEPTH * P2_NOPS * P2_T;
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 template <int NW>
 __device__ __forceinline__ double block_sum2d(double v, double* red, int warp, int lane) {
@@ -270,10 +291,12 @@ __device__ __forceinline__ double serial_sum2d(const double* prod, int n, double
 
 __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
   constexpr int NW = P2_T / 32;
+  extern __shared__ __align__(16) double dsm[];
   __shared__ LevelTab tab;
   __shared__ double sbuf[2][P2_T + 2];   // previous level of the running sweep (index iy + 1)
   __shared__ double red[4][NW];
   __shared__ int64_t s_item;
+  __shared__ double s_bval;
   const Grid2D g = prm.g;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   build_levels(tab, g);
@@ -321,7 +344,7 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
     int xc = 0, pc = 0;  // current ping-pong halves
 
     // ---- setup: assemble the sample's rows, x = 0, r = b ----------------------
-    double bb_loc = 0.0, bval = 0.0;
+    double bb_loc = 0.0;
     for (int l = 0; l < g.L; ++l) {
       const int a = wf_addr(tab, g, l, t);
       if (a >= 0) {
@@ -331,43 +354,82 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
         As[a] = rc.s;
         Xb[0][a] = 0.0;
         Rv[a] = rc.b;
-        bval = rc.b;  // b_i = area_sum / 3 is the same for every interior node of this mesh
+        if (t == 0 && l == 0) s_bval = rc.b;  // b_i = area_sum / 3: the same for every interior node
         bb_loc = fma(rc.b, rc.b, bb_loc);
         if (exact) Prod[nat(l)] = __dmul_rn(rc.b, rc.b);
       }
     }
     __syncthreads();
+    // the flat passes below touch nodes of every thread, so b comes from one shared copy
+    const double bval = s_bval;
     const int max_iter = prm.max_iter_arr ? prm.max_iter_arr[gs] : (prm.max_iter < 0 ? 10 * n : prm.max_iter);
 
-    // z = M^{-1} r by the level-scheduled IC(0) sweeps (oracle arithmetic); returns the r.z partial
+    // z = M^{-1} r by the level-scheduled IC(0) sweeps (oracle arithmetic); returns the r.z partial.
+    // Each thread prefetches ITS OWN node's operands P2_DEPTH-1 levels ahead with
+    // cp.async into a shared-memory ring (no registers held; a thread only reads
+    // what it copied, so the ring needs no barrier), hiding the HBM latency that
+    // otherwise stalls every one of the 2 x (2m-1) dependent levels.
+    double (*ring)[P2_NOPS][P2_T] = reinterpret_cast<double (*)[P2_NOPS][P2_T]>(dsm);
+    auto fwd_issue = [&](int l) {
+      const int a = wf_addr(tab, g, l, t);
+      if (a >= 0) {
+        double* r0 = &ring[l % P2_DEPTH][0][t];
+        cp_async8(r0 + P2_T, FW + a);
+        cp_async8(r0 + 2 * P2_T, FS + a);
+        cp_async8(r0 + 3 * P2_T, FD + a);
+      }
+      cp_commit();
+    };
+    auto bwd_issue = [&](int l) {
+      const int a = wf_addr(tab, g, l, t);
+      if (a >= 0) {
+        double* r0 = &ring[l % P2_DEPTH][0][t];
+        const int ae = wf_addr(tab, g, l + 1, t), an = wf_addr(tab, g, l + 1, t + 1);
+        if (ae >= 0) cp_async8(r0, FW + ae);
+        if (an >= 0) cp_async8(r0 + P2_T, FS + an);
+        cp_async8(r0 + 2 * P2_T, FD + a);
+        cp_async8(r0 + 3 * P2_T, Y + a);
+      }
+      cp_commit();
+    };
     auto sweeps = [&]() -> double {
       // forward (D + L) y = r, ascending levels
       __syncthreads();
+      for (int l = 0; l < P2_DEPTH - 1; ++l) fwd_issue(l);
       for (int l = 0; l < g.L; ++l) {
+        fwd_issue(l + P2_DEPTH - 1);  // slot of level l-1, already consumed
+        cp_wait<P2_DEPTH - 1>();
         const int cur = l & 1, prv = cur ^ 1;
         const int a = wf_addr(tab, g, l, t);
         if (a >= 0) {
+          const double* op = &ring[l % P2_DEPTH][0][t];
           const int ix = l - t;
           double v = Rv[a];
-          if (ix > 0) v = __dsub_rn(v, __dmul_rn(FW[a], sbuf[prv][t + 1]));
-          if (t > 0) v = __dsub_rn(v, __dmul_rn(FS[a], sbuf[prv][t]));
-          v = __ddiv_rn(v, FD[a]);
+          if (ix > 0) v = __dsub_rn(v, __dmul_rn(op[P2_T], sbuf[prv][t + 1]));
+          if (t > 0) v = __dsub_rn(v, __dmul_rn(op[2 * P2_T], sbuf[prv][t]));
+          v = __ddiv_rn(v, op[3 * P2_T]);
           Y[a] = v;
           sbuf[cur][t + 1] = v;
         }
         __syncthreads();
       }
+      cp_wait<0>();
+      __syncthreads();  // Y complete before the backward prefetch reads it
       // backward (D + L^T) z = D y, descending levels: z_i = y_i - (aE z_E + aN z_N) / D_i
       double rz_part = 0.0;
+      for (int l = g.L - 1; l > g.L - P2_DEPTH; --l) bwd_issue(l);
       for (int l = g.L - 1; l >= 0; --l) {
+        bwd_issue(l - (P2_DEPTH - 1));
+        cp_wait<P2_DEPTH - 1>();
         const int cur = l & 1, prv = cur ^ 1;
         const int a = wf_addr(tab, g, l, t);
         if (a >= 0) {
+          const double* op = &ring[l % P2_DEPTH][0][t];
           const int ix = l - t;
           double acc = 0.0;
-          if (ix < g.m - 1) acc = __dadd_rn(acc, __dmul_rn(FW[wf_addr(tab, g, l + 1, t)], sbuf[prv][t + 1]));
-          if (t < g.m - 1) acc = __dadd_rn(acc, __dmul_rn(FS[wf_addr(tab, g, l + 1, t + 1)], sbuf[prv][t + 2]));
-          const double z = __dsub_rn(Y[a], __ddiv_rn(acc, FD[a]));
+          if (ix < g.m - 1) acc = __dadd_rn(acc, __dmul_rn(op[0], sbuf[prv][t + 1]));
+          if (t < g.m - 1) acc = __dadd_rn(acc, __dmul_rn(op[P2_T], sbuf[prv][t + 2]));
+          const double z = __dsub_rn(op[3 * P2_T], __ddiv_rn(acc, op[2 * P2_T]));
           Z[a] = z;
           sbuf[cur][t + 1] = z;
           rz_part = fma(Rv[a], z, rz_part);
@@ -375,6 +437,7 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
         }
         __syncthreads();
       }
+      cp_wait<0>();
       return rz_part;
     };
 
@@ -395,21 +458,19 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
         const bool first = j == 1;
         auto pnew = [&](int q) { return q < 0 ? 0.0 : (first ? Z[q] : __dadd_rn(Z[q], __dmul_rn(beta, Po[q]))); };
         double pap = 0.0;
-        for (int l = 0; l < g.L; ++l) {
-          const int a = wf_addr(tab, g, l, t);
-          if (a >= 0) {
-            const int ix = l - t;
-            const int aw = ix > 0 ? wf_addr(tab, g, l - 1, t) : -1;
-            const int as = t > 0 ? wf_addr(tab, g, l - 1, t - 1) : -1;
-            const int ae = ix < g.m - 1 ? wf_addr(tab, g, l + 1, t) : -1;
-            const int an = t < g.m - 1 ? wf_addr(tab, g, l + 1, t + 1) : -1;
-            const double pcv = pnew(a);
-            const double ap = row_apply(As[a], Aw[a], Ad[a], ae >= 0 ? Aw[ae] : 0.0, an >= 0 ? As[an] : 0.0,
-                                        pnew(as), pnew(aw), pcv, pnew(ae), pnew(an));
-            Pn[a] = pcv;
-            pap = fma(pcv, ap, pap);
-            if (exact) Prod[nat(l)] = __dmul_rn(pcv, ap);
-          }
+        // barrier-free: walk the wavefront array in flat chunks (all lanes busy)
+        for (int a = t; a < n; a += P2_T) {
+          const int lv = prm.gmap[a], l = lv & 0xffff, iy = lv >> 16, ix = l - iy;
+          const int aw = ix > 0 ? a - tab.dw[l] : -1;
+          const int as = iy > 0 ? a - tab.dw[l] - 1 : -1;
+          const int ae = ix < g.m - 1 ? a + tab.de[l] : -1;
+          const int an = iy < g.m - 1 ? a + tab.de[l] + 1 : -1;
+          const double pcv = pnew(a);
+          const double ap = row_apply(As[a], Aw[a], Ad[a], ae >= 0 ? Aw[ae] : 0.0, an >= 0 ? As[an] : 0.0,
+                                      pnew(as), pnew(aw), pcv, pnew(ae), pnew(an));
+          Pn[a] = pcv;
+          pap = fma(pcv, ap, pap);
+          if (exact) Prod[iy * g.m + ix] = __dmul_rn(pcv, ap);
         }
         pc ^= 1;
         const double pAp = reduce(pap, red[0]);
@@ -423,28 +484,25 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
         const double* Xo = Xb[xc];
         double* Xn = Xb[xc ^ 1];
         double rr = 0.0;
-        for (int l = 0; l < g.L; ++l) {
-          const int a = wf_addr(tab, g, l, t);
-          if (a >= 0) {
-            const int ix = l - t;
-            const int aw = ix > 0 ? wf_addr(tab, g, l - 1, t) : -1;
-            const int as = t > 0 ? wf_addr(tab, g, l - 1, t - 1) : -1;
-            const int ae = ix < g.m - 1 ? wf_addr(tab, g, l + 1, t) : -1;
-            const int an = t < g.m - 1 ? wf_addr(tab, g, l + 1, t + 1) : -1;
-            auto pv = [&](int q) { return q < 0 ? 0.0 : Pv[q]; };
-            // every x_new is recomputed with the operation its owner uses (bit-identical);
-            // updates follow solver.cpp:216-218/241 without contraction
-            auto xnew = [&](int q) { return q < 0 ? 0.0 : __dadd_rn(Xo[q], __dmul_rn(alpha, Pv[q])); };
-            const double aE = ae >= 0 ? Aw[ae] : 0.0, aN = an >= 0 ? As[an] : 0.0;
-            const double ap = row_apply(As[a], Aw[a], Ad[a], aE, aN, pv(as), pv(aw), Pv[a], pv(ae), pv(an));
-            const double xn = xnew(a);
-            const double ax = row_apply(As[a], Aw[a], Ad[a], aE, aN, xnew(as), xnew(aw), xn, xnew(ae), xnew(an));
-            const double rt = __dsub_rn(bval, ax);
-            rr = fma(rt, rt, rr);
-            if (exact) Prod[nat(l)] = __dmul_rn(rt, rt);
-            Xn[a] = xn;
-            Rv[a] = __dsub_rn(Rv[a], __dmul_rn(alpha, ap));
-          }
+        for (int a = t; a < n; a += P2_T) {
+          const int lv = prm.gmap[a], l = lv & 0xffff, iy = lv >> 16, ix = l - iy;
+          const int aw = ix > 0 ? a - tab.dw[l] : -1;
+          const int as = iy > 0 ? a - tab.dw[l] - 1 : -1;
+          const int ae = ix < g.m - 1 ? a + tab.de[l] : -1;
+          const int an = iy < g.m - 1 ? a + tab.de[l] + 1 : -1;
+          auto pv = [&](int q) { return q < 0 ? 0.0 : Pv[q]; };
+          // every x_new is recomputed with the operation its owner uses (bit-identical);
+          // updates follow solver.cpp:216-218/241 without contraction
+          auto xnew = [&](int q) { return q < 0 ? 0.0 : __dadd_rn(Xo[q], __dmul_rn(alpha, Pv[q])); };
+          const double aE = ae >= 0 ? Aw[ae] : 0.0, aN = an >= 0 ? As[an] : 0.0;
+          const double ap = row_apply(As[a], Aw[a], Ad[a], aE, aN, pv(as), pv(aw), Pv[a], pv(ae), pv(an));
+          const double xn = xnew(a);
+          const double ax = row_apply(As[a], Aw[a], Ad[a], aE, aN, xnew(as), xnew(aw), xn, xnew(ae), xnew(an));
+          const double rt = __dsub_rn(bval, ax);
+          rr = fma(rt, rt, rr);
+          if (exact) Prod[iy * g.m + ix] = __dmul_rn(rt, rt);
+          Xn[a] = xn;
+          Rv[a] = __dsub_rn(Rv[a], __dmul_rn(alpha, ap));
         }
         xc ^= 1;
         const double rel = sqrt(reduce(rr, red[1])) / norm_b;
@@ -477,6 +535,16 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
       }
     }
     __syncthreads();
+  }
+}
+
+// per wavefront address: level | (iy << 16) (shared by every sample of the grid)
+__global__ void __launch_bounds__(P2_T) build_gmap_kernel(const Grid2D g, int* gmap) {
+  __shared__ LevelTab tab;
+  build_levels(tab, g);
+  for (int l = blockIdx.x; l < g.L; l += gridDim.x) {
+    const int lo = tab.lo[l], hi = lvl_hi(l, g.m);
+    for (int iy = lo + threadIdx.x; iy <= hi; iy += blockDim.x) gmap[tab.off[l] + iy - lo] = l | (iy << 16);
   }
 }
 

@@ -96,6 +96,7 @@ struct vqpc_ctx {
   // 2-D path: grid, IC(0) factors (P x 3n, wavefront order), per-CTA PCG scratch
   Grid2D g2{};
   DBuf<double> fac2, work2;
+  DBuf<int> gmap;
   int exact = 0;  // 2-D: serial (reference-order) dot products
   // work buffers
   DBuf<double> xi, kappa, best, dvec;
@@ -258,10 +259,11 @@ void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d
                const int32_t* d_labels, int64_t B, int64_t out_base, double eps, int max_iter, const int32_t* d_mia,
                int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x, int64_t solve_limit) {
   int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg2d_kernel, P2_T, 0));
+  CK(cudaFuncSetAttribute(pcg2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P2_DSMEM)));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg2d_kernel, P2_T, P2_DSMEM));
   if (per_sm < 1) throw ApiError{VQPC_CUDA_ERROR, "pcg2d kernel does not fit on an SM"};
-  const int64_t slots = std::min<int64_t>(B, static_cast<int64_t>(per_sm) * c->sm_count);
-  c->work2.ensure(static_cast<size_t>(slots) * P2_WORK * c->n);
+  const int64_t blocks = std::min<int64_t>(B, static_cast<int64_t>(per_sm) * c->sm_count);
+  c->work2.ensure(static_cast<size_t>(blocks) * P2_WORK * c->n);
   c->counter.ensure(1);
   CK(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->stream));
   Pcg2dParams prm{};
@@ -285,8 +287,14 @@ void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d
   prm.status = d_status;
   prm.x_out = d_x;
   prm.exact = c->exact;
+  if (!c->gmap.p) {
+    c->gmap.ensure(c->n);
+    build_gmap_kernel<<<64, P2_T, 0, c->stream>>>(c->g2, c->gmap.p);
+    launch_check(c);
+  }
+  prm.gmap = c->gmap.p;
   Timed tm(c, VQPC_K_PCG);
-  pcg2d_kernel<<<static_cast<unsigned>(slots), P2_T, 0, c->stream>>>(prm);
+  pcg2d_kernel<<<static_cast<unsigned>(blocks), P2_T, P2_DSMEM, c->stream>>>(prm);
   launch_check(c);
 }
 
@@ -564,6 +572,7 @@ void vqpc_ctx_destroy(vqpc_ctx* c) {
   c->stats.release();
   c->counter.release();
   c->err.release();
+  c->gmap.release();
   for (auto& r : c->recs) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
