@@ -246,11 +246,27 @@ struct Pcg2dParams {
 constexpr int P2_WORK = 11;  // per-CTA scratch vectors: d, w, s, x[2], r, p[2], y, z, prod
 constexpr int P2_DEPTH = 6;  // cp.async prefetch ring depth (levels) for the IC(0) sweeps
 constexpr int P2_NOPS = 5;   // operands per node in the ring
-constexpr size_t P2_DSMEM = sizeof(double) * P2_DEPTH * P2_NOPS * P2_T;
+// Flat passes (P1, P2) stream the wavefront array in chunks of P2_T addresses:
+// each thread prefetches its own address of chunk k + P2_SD with cp.async into
+// a raw slot only it reads, and publishes the values its neighbours need into
+// 4-slot exchange rings (a node's neighbours lie in chunks k-1..k+1 since a
+// level holds <= P2_T - 1 nodes). One barrier per chunk.
+constexpr int P2_SD = 3;       // chunks in flight
+constexpr int P2_RAW = 6;      // raw double vectors per address
+constexpr int P2_XCH = 4;      // exchange rings
+constexpr size_t P2_RING_SM = sizeof(double) * P2_DEPTH * P2_NOPS * P2_T;
+constexpr size_t P2_FLAT_SM = sizeof(double) * (4 * P2_RAW + 4 * P2_XCH) * P2_T + sizeof(int) * 4 * P2_T;
+constexpr size_t P2_DSMEM = P2_RING_SM > P2_FLAT_SM ? P2_RING_SM : P2_FLAT_SM;
+static_assert(P2_T == 256, "chunk indexing assumes 256-address chunks");
+static_assert(P2_SD + 1 == 4, "raw slots: the slot refilled in step k is the one read in step k-1");
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -374,6 +390,7 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
       const int a = wf_addr(tab, g, l, t);
       if (a >= 0) {
         double* r0 = &ring[l % P2_DEPTH][0][t];
+        cp_async8(r0, Rv + a);
         cp_async8(r0 + P2_T, FW + a);
         cp_async8(r0 + 2 * P2_T, FS + a);
         cp_async8(r0 + 3 * P2_T, FD + a);
@@ -389,6 +406,7 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
         if (an >= 0) cp_async8(r0 + P2_T, FS + an);
         cp_async8(r0 + 2 * P2_T, FD + a);
         cp_async8(r0 + 3 * P2_T, Y + a);
+        cp_async8(r0 + 4 * P2_T, Rv + a);
       }
       cp_commit();
     };
@@ -404,7 +422,7 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
         if (a >= 0) {
           const double* op = &ring[l % P2_DEPTH][0][t];
           const int ix = l - t;
-          double v = Rv[a];
+          double v = op[0];
           if (ix > 0) v = __dsub_rn(v, __dmul_rn(op[P2_T], sbuf[prv][t + 1]));
           if (t > 0) v = __dsub_rn(v, __dmul_rn(op[2 * P2_T], sbuf[prv][t]));
           v = __ddiv_rn(v, op[3 * P2_T]);
@@ -432,8 +450,8 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
           const double z = __dsub_rn(op[3 * P2_T], __ddiv_rn(acc, op[2 * P2_T]));
           Z[a] = z;
           sbuf[cur][t + 1] = z;
-          rz_part = fma(Rv[a], z, rz_part);
-          if (exact) Prod[nat(l)] = __dmul_rn(Rv[a], z);
+          rz_part = fma(op[4 * P2_T], z, rz_part);
+          if (exact) Prod[nat(l)] = __dmul_rn(op[4 * P2_T], z);
         }
         __syncthreads();
       }
@@ -452,25 +470,79 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
     else {
       double beta = 0.0;
       for (int j = 1; j <= max_iter; ++j) {
-        // ---- P1 (barrier-free): p_new = z + beta p_old into the other half; pAp -----
+        // ---- P1: p_new = z + beta p_old into the other half; pAp (chunk-streamed) ----
         const double* Po = Pb[pc];
         double* Pn = Pb[pc ^ 1];
         const bool first = j == 1;
-        auto pnew = [&](int q) { return q < 0 ? 0.0 : (first ? Z[q] : __dadd_rn(Z[q], __dmul_rn(beta, Po[q]))); };
+        const int NC = (n + P2_T - 1) / P2_T;
+        double* raw = dsm;                                   // [4][P2_RAW][P2_T]
+        double* xch = dsm + 4 * P2_RAW * P2_T;               // [P2_XCH][4][P2_T]
+        int* rawi = reinterpret_cast<int*>(xch + 4 * P2_XCH * P2_T);  // [4][P2_T]
+        auto RAW = [&](int k, int v) -> double* { return raw + ((k & 3) * P2_RAW + v) * P2_T + t; };
+        auto XCH = [&](int x, int q) -> double& { return xch[(x * 4 + ((q >> 8) & 3)) * P2_T + (q & (P2_T - 1))]; };
+        auto flat_issue = [&](int k, const double* v0, const double* v1, const double* v2) {
+          const int a = k * P2_T + t;
+          if (k < NC && a < n) {
+            if (v0) cp_async8(RAW(k, 0), v0 + a);
+            if (v1) cp_async8(RAW(k, 1), v1 + a);
+            if (v2) cp_async8(RAW(k, 2), v2 + a);
+            cp_async8(RAW(k, 3), As + a);
+            cp_async8(RAW(k, 4), Aw + a);
+            cp_async8(RAW(k, 5), Ad + a);
+            cp_async4(rawi + (k & 3) * P2_T + t, prm.gmap + a);
+          }
+          cp_commit();
+        };
+        // neighbour addresses of wavefront address a (level l, row iy); -1 off the mesh
+        struct Nb { int s, w, e, nn, ix, iy; };
+        auto nbrs = [&](int a, int lv) {
+          const int l = lv & 0xffff, iy = lv >> 16, ix = l - iy;
+          Nb b;
+          b.w = ix > 0 ? a - tab.dw[l] : -1;
+          b.s = iy > 0 ? a - tab.dw[l] - 1 : -1;
+          b.e = ix < g.m - 1 ? a + tab.de[l] : -1;
+          b.nn = iy < g.m - 1 ? a + tab.de[l] + 1 : -1;
+          b.ix = ix;
+          b.iy = iy;
+          return b;
+        };
+        auto xv = [&](int x, int q) { return q < 0 ? 0.0 : XCH(x, q); };
         double pap = 0.0;
-        // barrier-free: walk the wavefront array in flat chunks (all lanes busy)
-        for (int a = t; a < n; a += P2_T) {
-          const int lv = prm.gmap[a], l = lv & 0xffff, iy = lv >> 16, ix = l - iy;
-          const int aw = ix > 0 ? a - tab.dw[l] : -1;
-          const int as = iy > 0 ? a - tab.dw[l] - 1 : -1;
-          const int ae = ix < g.m - 1 ? a + tab.de[l] : -1;
-          const int an = iy < g.m - 1 ? a + tab.de[l] + 1 : -1;
-          const double pcv = pnew(a);
-          const double ap = row_apply(As[a], Aw[a], Ad[a], ae >= 0 ? Aw[ae] : 0.0, an >= 0 ? As[an] : 0.0,
-                                      pnew(as), pnew(aw), pcv, pnew(ae), pnew(an));
-          Pn[a] = pcv;
-          pap = fma(pcv, ap, pap);
-          if (exact) Prod[iy * g.m + ix] = __dmul_rn(pcv, ap);
+        {
+          for (int k = 0; k < P2_SD; ++k) flat_issue(k, Z, first ? nullptr : Po, nullptr);
+          double cs = 0.0, cw = 0.0, cd = 0.0;
+          int clv = 0;
+          for (int k = 0; k <= NC; ++k) {
+            const double ps = cs, pw = cw, pd = cd;
+            const int plv = clv;
+            if (k < NC) {
+              cp_wait<P2_SD - 1>();
+              const int a = k * P2_T + t;
+              if (a < n) {
+                const double z = *RAW(k, 0);
+                const double pcv = first ? z : __dadd_rn(z, __dmul_rn(beta, *RAW(k, 1)));
+                cs = *RAW(k, 3);
+                cw = *RAW(k, 4);
+                cd = *RAW(k, 5);
+                clv = rawi[(k & 3) * P2_T + t];
+                XCH(0, a) = pcv;
+                XCH(2, a) = cw;
+                XCH(3, a) = cs;
+                Pn[a] = pcv;
+              }
+            }
+            flat_issue(k + P2_SD, Z, first ? nullptr : Po, nullptr);
+            __syncthreads();
+            const int a = (k - 1) * P2_T + t;
+            if (k >= 1 && a < n) {
+              const Nb b = nbrs(a, plv);
+              const double pcv = XCH(0, a);
+              const double ap = row_apply(ps, pw, pd, xv(2, b.e), xv(3, b.nn), xv(0, b.s), xv(0, b.w), pcv,
+                                          xv(0, b.e), xv(0, b.nn));
+              pap = fma(pcv, ap, pap);
+              if (exact) Prod[b.iy * g.m + b.ix] = __dmul_rn(pcv, ap);
+            }
+          }
         }
         pc ^= 1;
         const double pAp = reduce(pap, red[0]);
@@ -479,30 +551,54 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
           break;
         }
         const double alpha = rz / pAp;
-        // ---- P2 (barrier-free): x_new = x + alpha p, r -= alpha A p, |b - A x_new|^2 ---
+        // ---- P2: x_new = x + alpha p, r -= alpha A p, |b - A x_new|^2 (chunk-streamed) --
+        // every x_new is recomputed with the operation its owner uses (bit-identical);
+        // updates follow solver.cpp:216-218/241 without contraction
         const double* Pv = Pb[pc];
         const double* Xo = Xb[xc];
         double* Xn = Xb[xc ^ 1];
         double rr = 0.0;
-        for (int a = t; a < n; a += P2_T) {
-          const int lv = prm.gmap[a], l = lv & 0xffff, iy = lv >> 16, ix = l - iy;
-          const int aw = ix > 0 ? a - tab.dw[l] : -1;
-          const int as = iy > 0 ? a - tab.dw[l] - 1 : -1;
-          const int ae = ix < g.m - 1 ? a + tab.de[l] : -1;
-          const int an = iy < g.m - 1 ? a + tab.de[l] + 1 : -1;
-          auto pv = [&](int q) { return q < 0 ? 0.0 : Pv[q]; };
-          // every x_new is recomputed with the operation its owner uses (bit-identical);
-          // updates follow solver.cpp:216-218/241 without contraction
-          auto xnew = [&](int q) { return q < 0 ? 0.0 : __dadd_rn(Xo[q], __dmul_rn(alpha, Pv[q])); };
-          const double aE = ae >= 0 ? Aw[ae] : 0.0, aN = an >= 0 ? As[an] : 0.0;
-          const double ap = row_apply(As[a], Aw[a], Ad[a], aE, aN, pv(as), pv(aw), Pv[a], pv(ae), pv(an));
-          const double xn = xnew(a);
-          const double ax = row_apply(As[a], Aw[a], Ad[a], aE, aN, xnew(as), xnew(aw), xn, xnew(ae), xnew(an));
-          const double rt = __dsub_rn(bval, ax);
-          rr = fma(rt, rt, rr);
-          if (exact) Prod[iy * g.m + ix] = __dmul_rn(rt, rt);
-          Xn[a] = xn;
-          Rv[a] = __dsub_rn(Rv[a], __dmul_rn(alpha, ap));
+        {
+          for (int k = 0; k < P2_SD; ++k) flat_issue(k, Pv, Xo, Rv);
+          double cs = 0.0, cw = 0.0, cd = 0.0, cr = 0.0;
+          int clv = 0;
+          for (int k = 0; k <= NC; ++k) {
+            const double ps = cs, pw = cw, pd = cd, pr = cr;
+            const int plv = clv;
+            if (k < NC) {
+              cp_wait<P2_SD - 1>();
+              const int a = k * P2_T + t;
+              if (a < n) {
+                const double pvv = *RAW(k, 0);
+                const double xn = __dadd_rn(*RAW(k, 1), __dmul_rn(alpha, pvv));
+                cr = *RAW(k, 2);
+                cs = *RAW(k, 3);
+                cw = *RAW(k, 4);
+                cd = *RAW(k, 5);
+                clv = rawi[(k & 3) * P2_T + t];
+                XCH(0, a) = pvv;
+                XCH(1, a) = xn;
+                XCH(2, a) = cw;
+                XCH(3, a) = cs;
+                Xn[a] = xn;
+              }
+            }
+            flat_issue(k + P2_SD, Pv, Xo, Rv);
+            __syncthreads();
+            const int a = (k - 1) * P2_T + t;
+            if (k >= 1 && a < n) {
+              const Nb b = nbrs(a, plv);
+              const double aE = xv(2, b.e), aN = xv(3, b.nn);
+              const double ap = row_apply(ps, pw, pd, aE, aN, xv(0, b.s), xv(0, b.w), XCH(0, a), xv(0, b.e),
+                                          xv(0, b.nn));
+              const double ax = row_apply(ps, pw, pd, aE, aN, xv(1, b.s), xv(1, b.w), XCH(1, a), xv(1, b.e),
+                                          xv(1, b.nn));
+              const double rt = __dsub_rn(bval, ax);
+              rr = fma(rt, rt, rr);
+              if (exact) Prod[b.iy * g.m + b.ix] = __dmul_rn(rt, rt);
+              Rv[a] = __dsub_rn(pr, __dmul_rn(alpha, ap));
+            }
+          }
         }
         xc ^= 1;
         const double rel = sqrt(reduce(rr, red[1])) / norm_b;
