@@ -178,6 +178,11 @@ int vqpc_profile_read(vqpc_ctx* ctx, double* ms, int64_t* counts, int reset);
  * the achieved fp64 TFLOP/s (2 flops per FMA) measured with CUDA events. */
 int vqpc_fp64_peak(int device, double* tflops);
 
+/* Diagnostics: cycles spent by the 2-D PCG in setup, IC(0) sweeps, P1 and P2,
+ * summed over CTAs (all zero unless the library was built with
+ * -DVQPC_PHASE_TIMING). */
+int vqpc_debug_pcg2d_phase_cycles(unsigned long long* out4, int reset);
+
 /* ---- quantizer construction on the host with device assignment sweeps ----
  * kmeans = minmax seeding + Lloyd (quantizer.cpp:181-357), bit-identical to
  * the reference (labels and distances are exact; means are summed on the

@@ -176,12 +176,42 @@ __device__ inline void build_levels(LevelTab& tab, const Grid2D g) {
   __syncthreads();
 }
 
-// address of node (l - t, t) in wavefront order, or -1 if not on level l
-__device__ __forceinline__ int wf_addr(const LevelTab& tab, const Grid2D g, int l, int t) {
-  if (l < 0 || l >= g.L) return -1;
-  const int lo = tab.lo[l], hi = lvl_hi(l, g.m);
-  return (t >= lo && t <= hi) ? tab.off[l] + t - lo : -1;
+// address of node (l - t, t) in wavefront order, or -1 if not on level l.
+// Closed form (no table lookups on the sweeps' critical path): levels l < m hold
+// l + 1 nodes, levels l >= m hold 2m - 1 - l, so off(l) = l(l+1)/2 below m and
+// m^2 - r(r+1)/2 with r = 2m - 1 - l above.
+__device__ __forceinline__ int wf_addr(const Grid2D g, int l, int t) {
+  const int m = g.m;
+  if (static_cast<unsigned>(l) >= static_cast<unsigned>(g.L)) return -1;
+  int off, lo, hi;
+  if (l < m) {
+    off = (l * (l + 1)) >> 1;
+    lo = 0;
+    hi = l;
+  } else {
+    const int r = 2 * m - 1 - l;
+    off = m * m - ((r * (r + 1)) >> 1);
+    lo = l - m + 1;
+    hi = m - 1;
+  }
+  return (t >= lo && t <= hi) ? off + t - lo : -1;
 }
+__device__ __forceinline__ int wf_addr(const LevelTab&, const Grid2D g, int l, int t) { return wf_addr(g, l, t); }
+
+__device__ __forceinline__ int wf_size(int l, int m) { return l < m ? l + 1 : 2 * m - 1 - l; }
+// a - a_W for the nodes of level l (a_S = a_W - 1), and a_E - a (a_N = a_E + 1)
+__device__ __forceinline__ int wf_dw(int l, int m) { return wf_size(l - 1, m) + lvl_lo(l - 1, m) - lvl_lo(l, m); }
+__device__ __forceinline__ int wf_de(int l, int m) { return wf_size(l, m) + lvl_lo(l, m) - lvl_lo(l + 1, m); }
+
+#ifdef VQPC_PHASE_TIMING
+__device__ unsigned long long g_pcg2d_phase[4];  // cycles: setup, sweeps, P1, P2 (CTA thread 0)
+#define P2_TIC(v) const long long v = clock64()
+#define P2_TOC(i, v) \
+  if (threadIdx.x == 0) atomicAdd(&g_pcg2d_phase[i], static_cast<unsigned long long>(clock64() - v))
+#else
+#define P2_TIC(v)
+#define P2_TOC(i, v)
+#endif
 
 // ---- (e) IC(0) factor of every centroid matrix (one CTA per centroid) ---------
 // fac layout per centroid (3 n doubles, wavefront order): D, aW, aS of A_c.
@@ -244,21 +274,25 @@ struct Pcg2dParams {
 };
 
 constexpr int P2_WORK = 11;  // per-CTA scratch vectors: d, w, s, x[2], r, p[2], y, z, prod
-constexpr int P2_DEPTH = 6;  // cp.async prefetch ring depth (levels) for the IC(0) sweeps
+#ifndef P2_DEPTH_OVERRIDE
+constexpr int P2_DEPTH = 6;
+#else
+constexpr int P2_DEPTH = P2_DEPTH_OVERRIDE;
+#endif  // cp.async prefetch ring depth (levels) for the IC(0) sweeps
 constexpr int P2_NOPS = 5;   // operands per node in the ring
 // Flat passes (P1, P2) stream the wavefront array in chunks of P2_T addresses:
 // each thread prefetches its own address of chunk k + P2_SD with cp.async into
-// a raw slot only it reads, and publishes the values its neighbours need into
-// 4-slot exchange rings (a node's neighbours lie in chunks k-1..k+1 since a
+// a raw slot only it reads, and publishes the vector values its neighbours need
+// into 4-slot exchange rings (a node's neighbours lie in chunks k-1..k+1 since a
 // level holds <= P2_T - 1 nodes). One barrier per chunk.
 constexpr int P2_SD = 3;       // chunks in flight
+constexpr int P2_RSLOT = P2_SD + 1;  // raw slots: the slot refilled in step k is the one read in step k-1
 constexpr int P2_RAW = 6;      // raw double vectors per address
-constexpr int P2_XCH = 4;      // exchange rings
+constexpr int P2_XCH = 4;      // exchange rings: p (or p_new), x_new, aW, aS; 4 chunk slots each (k-2..k+1 live)
 constexpr size_t P2_RING_SM = sizeof(double) * P2_DEPTH * P2_NOPS * P2_T;
-constexpr size_t P2_FLAT_SM = sizeof(double) * (4 * P2_RAW + 4 * P2_XCH) * P2_T + sizeof(int) * 4 * P2_T;
+constexpr size_t P2_FLAT_SM = sizeof(double) * (P2_RSLOT * P2_RAW + 4 * P2_XCH) * P2_T + sizeof(int) * P2_RSLOT * P2_T;
 constexpr size_t P2_DSMEM = P2_RING_SM > P2_FLAT_SM ? P2_RING_SM : P2_FLAT_SM;
 static_assert(P2_T == 256, "chunk indexing assumes 256-address chunks");
-static_assert(P2_SD + 1 == 4, "raw slots: the slot refilled in step k is the one read in step k-1");
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -305,17 +339,15 @@ __device__ __forceinline__ double serial_sum2d(const double* prod, int n, double
   return v;
 }
 
-__global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
+__global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
   constexpr int NW = P2_T / 32;
   extern __shared__ __align__(16) double dsm[];
-  __shared__ LevelTab tab;
-  __shared__ double sbuf[2][P2_T + 2];   // previous level of the running sweep (index iy + 1)
+  __shared__ double sbuf[2][P2_T + 2];  // previous level of the running sweep (index iy + 1)
   __shared__ double red[4][NW];
   __shared__ int64_t s_item;
   __shared__ double s_bval;
   const Grid2D g = prm.g;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  build_levels(tab, g);
   const int n = g.n;
   double* base = prm.work + static_cast<size_t>(blockIdx.x) * P2_WORK * n;
   double* Ad = base;          // diagonal
@@ -362,7 +394,7 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
     // ---- setup: assemble the sample's rows, x = 0, r = b ----------------------
     double bb_loc = 0.0;
     for (int l = 0; l < g.L; ++l) {
-      const int a = wf_addr(tab, g, l, t);
+      const int a = wf_addr(g, l, t);
       if (a >= 0) {
         const RowCoef rc = assemble_row(kap, g, l - t, t);
         Ad[a] = rc.d;
@@ -386,9 +418,20 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
     // what it copied, so the ring needs no barrier), hiding the HBM latency that
     // otherwise stalls every one of the 2 x (2m-1) dependent levels.
     double (*ring)[P2_NOPS][P2_T] = reinterpret_cast<double (*)[P2_NOPS][P2_T]>(dsm);
-    auto fwd_issue = [&](int l) {
-      const int a = wf_addr(tab, g, l, t);
-      if (a >= 0) {
+    // Per-thread address cursors (no per-level table lookups): lin(l) is the
+    // wavefront address of row t on level l (linear in t, valid or not), up(l) =
+    // lin(l+1) - lin(l); row t has a node on level l iff 0 <= l - t < m.
+    const int m = g.m;
+    const bool trow = t < m;
+    auto lin = [&](int l) {
+      if (l < m) return ((l * (l + 1)) >> 1) + t;
+      const int r = 2 * m - 1 - l;
+      return m * m - ((r * (r + 1)) >> 1) + t - (l - m + 1);
+    };
+    auto up = [&](int l) { return l < m - 1 ? l + 1 : 2 * m - 2 - l; };
+    auto on = [&](int l) { return trow && static_cast<unsigned>(l - t) < static_cast<unsigned>(m); };
+    auto fwd_issue = [&](int l, int a) {
+      if (on(l)) {
         double* r0 = &ring[l % P2_DEPTH][0][t];
         cp_async8(r0, Rv + a);
         cp_async8(r0 + P2_T, FW + a);
@@ -397,13 +440,12 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
       }
       cp_commit();
     };
-    auto bwd_issue = [&](int l) {
-      const int a = wf_addr(tab, g, l, t);
-      if (a >= 0) {
+    auto bwd_issue = [&](int l, int a) {
+      if (l >= 0 && on(l)) {
         double* r0 = &ring[l % P2_DEPTH][0][t];
-        const int ae = wf_addr(tab, g, l + 1, t), an = wf_addr(tab, g, l + 1, t + 1);
-        if (ae >= 0) cp_async8(r0, FW + ae);
-        if (an >= 0) cp_async8(r0 + P2_T, FS + an);
+        const int ae = a + up(l);  // (ix+1, iy) on level l+1; (ix, iy+1) is the next address
+        if (l - t < m - 1) cp_async8(r0, FW + ae);
+        if (t < m - 1) cp_async8(r0 + P2_T, FS + ae + 1);
         cp_async8(r0 + 2 * P2_T, FD + a);
         cp_async8(r0 + 3 * P2_T, Y + a);
         cp_async8(r0 + 4 * P2_T, Rv + a);
@@ -413,46 +455,55 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
     auto sweeps = [&]() -> double {
       // forward (D + L) y = r, ascending levels
       __syncthreads();
-      for (int l = 0; l < P2_DEPTH - 1; ++l) fwd_issue(l);
+      int ai = lin(0), ac = ai;  // issue / compute cursors
+      for (int l = 0; l < P2_DEPTH - 1; ++l) {
+        fwd_issue(l, ai);
+        ai += up(l);
+      }
       for (int l = 0; l < g.L; ++l) {
-        fwd_issue(l + P2_DEPTH - 1);  // slot of level l-1, already consumed
+        fwd_issue(l + P2_DEPTH - 1, ai);  // slot of level l-1, already consumed
+        ai += up(l + P2_DEPTH - 1);
         cp_wait<P2_DEPTH - 1>();
         const int cur = l & 1, prv = cur ^ 1;
-        const int a = wf_addr(tab, g, l, t);
-        if (a >= 0) {
+        if (on(l)) {
           const double* op = &ring[l % P2_DEPTH][0][t];
-          const int ix = l - t;
           double v = op[0];
-          if (ix > 0) v = __dsub_rn(v, __dmul_rn(op[P2_T], sbuf[prv][t + 1]));
+          if (l - t > 0) v = __dsub_rn(v, __dmul_rn(op[P2_T], sbuf[prv][t + 1]));
           if (t > 0) v = __dsub_rn(v, __dmul_rn(op[2 * P2_T], sbuf[prv][t]));
           v = __ddiv_rn(v, op[3 * P2_T]);
-          Y[a] = v;
+          Y[ac] = v;
           sbuf[cur][t + 1] = v;
         }
+        ac += up(l);
         __syncthreads();
       }
       cp_wait<0>();
       __syncthreads();  // Y complete before the backward prefetch reads it
       // backward (D + L^T) z = D y, descending levels: z_i = y_i - (aE z_E + aN z_N) / D_i
       double rz_part = 0.0;
-      for (int l = g.L - 1; l > g.L - P2_DEPTH; --l) bwd_issue(l);
+      ai = lin(g.L - 1);
+      ac = ai;
+      for (int l = g.L - 1; l > g.L - P2_DEPTH; --l) {
+        bwd_issue(l, ai);
+        ai -= up(l - 1);
+      }
       for (int l = g.L - 1; l >= 0; --l) {
-        bwd_issue(l - (P2_DEPTH - 1));
+        bwd_issue(l - (P2_DEPTH - 1), ai);
+        ai -= up(l - P2_DEPTH);
         cp_wait<P2_DEPTH - 1>();
         const int cur = l & 1, prv = cur ^ 1;
-        const int a = wf_addr(tab, g, l, t);
-        if (a >= 0) {
+        if (on(l)) {
           const double* op = &ring[l % P2_DEPTH][0][t];
-          const int ix = l - t;
           double acc = 0.0;
-          if (ix < g.m - 1) acc = __dadd_rn(acc, __dmul_rn(op[0], sbuf[prv][t + 1]));
-          if (t < g.m - 1) acc = __dadd_rn(acc, __dmul_rn(op[P2_T], sbuf[prv][t + 2]));
+          if (l - t < m - 1) acc = __dadd_rn(acc, __dmul_rn(op[0], sbuf[prv][t + 1]));
+          if (t < m - 1) acc = __dadd_rn(acc, __dmul_rn(op[P2_T], sbuf[prv][t + 2]));
           const double z = __dsub_rn(op[3 * P2_T], __ddiv_rn(acc, op[2 * P2_T]));
-          Z[a] = z;
+          Z[ac] = z;
           sbuf[cur][t + 1] = z;
           rz_part = fma(op[4 * P2_T], z, rz_part);
-          if (exact) Prod[nat(l)] = __dmul_rn(op[4 * P2_T], z);
+          if (exact) Prod[t * m + (l - t)] = __dmul_rn(op[4 * P2_T], z);
         }
+        ac -= up(l - 1);
         __syncthreads();
       }
       cp_wait<0>();
@@ -471,14 +522,15 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
       double beta = 0.0;
       for (int j = 1; j <= max_iter; ++j) {
         // ---- P1: p_new = z + beta p_old into the other half; pAp (chunk-streamed) ----
+        P2_TIC(t_p1);
         const double* Po = Pb[pc];
         double* Pn = Pb[pc ^ 1];
         const bool first = j == 1;
         const int NC = (n + P2_T - 1) / P2_T;
-        double* raw = dsm;                                   // [4][P2_RAW][P2_T]
-        double* xch = dsm + 4 * P2_RAW * P2_T;               // [P2_XCH][4][P2_T]
-        int* rawi = reinterpret_cast<int*>(xch + 4 * P2_XCH * P2_T);  // [4][P2_T]
-        auto RAW = [&](int k, int v) -> double* { return raw + ((k & 3) * P2_RAW + v) * P2_T + t; };
+        double* raw = dsm;                                   // [P2_RSLOT][P2_RAW][P2_T]
+        double* xch = dsm + P2_RSLOT * P2_RAW * P2_T;        // [P2_XCH][4][P2_T]
+        int* rawi = reinterpret_cast<int*>(xch + 4 * P2_XCH * P2_T);  // [P2_RSLOT][P2_T]
+        auto RAW = [&](int k, int v) -> double* { return raw + ((k % P2_RSLOT) * P2_RAW + v) * P2_T + t; };
         auto XCH = [&](int x, int q) -> double& { return xch[(x * 4 + ((q >> 8) & 3)) * P2_T + (q & (P2_T - 1))]; };
         auto flat_issue = [&](int k, const double* v0, const double* v1, const double* v2) {
           const int a = k * P2_T + t;
@@ -489,7 +541,7 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
             cp_async8(RAW(k, 3), As + a);
             cp_async8(RAW(k, 4), Aw + a);
             cp_async8(RAW(k, 5), Ad + a);
-            cp_async4(rawi + (k & 3) * P2_T + t, prm.gmap + a);
+            cp_async4(rawi + (k % P2_RSLOT) * P2_T + t, prm.gmap + a);
           }
           cp_commit();
         };
@@ -498,10 +550,11 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
         auto nbrs = [&](int a, int lv) {
           const int l = lv & 0xffff, iy = lv >> 16, ix = l - iy;
           Nb b;
-          b.w = ix > 0 ? a - tab.dw[l] : -1;
-          b.s = iy > 0 ? a - tab.dw[l] - 1 : -1;
-          b.e = ix < g.m - 1 ? a + tab.de[l] : -1;
-          b.nn = iy < g.m - 1 ? a + tab.de[l] + 1 : -1;
+          const int dw = wf_dw(l, g.m), de = wf_de(l, g.m);
+          b.w = ix > 0 ? a - dw : -1;
+          b.s = iy > 0 ? a - dw - 1 : -1;
+          b.e = ix < g.m - 1 ? a + de : -1;
+          b.nn = iy < g.m - 1 ? a + de + 1 : -1;
           b.ix = ix;
           b.iy = iy;
           return b;
@@ -524,7 +577,7 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
                 cs = *RAW(k, 3);
                 cw = *RAW(k, 4);
                 cd = *RAW(k, 5);
-                clv = rawi[(k & 3) * P2_T + t];
+                clv = rawi[(k % P2_RSLOT) * P2_T + t];
                 XCH(0, a) = pcv;
                 XCH(2, a) = cw;
                 XCH(3, a) = cs;
@@ -546,12 +599,14 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
         }
         pc ^= 1;
         const double pAp = reduce(pap, red[0]);
+        P2_TOC(2, t_p1);
         if (!(pAp > 0.0)) {
           st = VQPC_S_BREAKDOWN;
           break;
         }
         const double alpha = rz / pAp;
         // ---- P2: x_new = x + alpha p, r -= alpha A p, |b - A x_new|^2 (chunk-streamed) --
+        P2_TIC(t_p2);
         // every x_new is recomputed with the operation its owner uses (bit-identical);
         // updates follow solver.cpp:216-218/241 without contraction
         const double* Pv = Pb[pc];
@@ -575,7 +630,7 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
                 cs = *RAW(k, 3);
                 cw = *RAW(k, 4);
                 cd = *RAW(k, 5);
-                clv = rawi[(k & 3) * P2_T + t];
+                clv = rawi[(k % P2_RSLOT) * P2_T + t];
                 XCH(0, a) = pvv;
                 XCH(1, a) = xn;
                 XCH(2, a) = cw;
@@ -602,6 +657,7 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
         }
         xc ^= 1;
         const double rel = sqrt(reduce(rr, red[1])) / norm_b;
+        P2_TOC(3, t_p2);
         J = j;
         rel_rec = rel;
         if (rel < prm.eps) {
@@ -609,7 +665,9 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
           break;
         }
         // ---- P3: z = M^{-1} r; r.z (level-ordered sweeps) ---------------------------
+        P2_TIC(t_sw);
         const double rz_next = reduce(sweeps(), red[2]);
+        P2_TOC(1, t_sw);
         if (!(rz_next > 0.0)) {
           st = VQPC_S_BREAKDOWN;
           break;
@@ -626,7 +684,7 @@ __global__ void __launch_bounds__(P2_T) pcg2d_kernel(const Pcg2dParams prm) {
     if (prm.x_out) {
       double* xo = prm.x_out + static_cast<size_t>(gs) * n;
       for (int l = 0; l < g.L; ++l) {
-        const int a = wf_addr(tab, g, l, t);
+        const int a = wf_addr(g, l, t);
         if (a >= 0) xo[t * g.m + (l - t)] = Xb[xc][a];
       }
     }

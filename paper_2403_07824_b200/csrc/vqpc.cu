@@ -860,3 +860,21 @@ int vqpc_run_campaign(vqpc_ctx* c, const double* xi, int64_t B, int ld, double e
 }
 
 }  // extern "C"
+
+// Diagnostics: per-phase cycles of the 2-D PCG (setup, sweeps, P1, P2), summed
+// over CTAs by thread 0; nonzero only in a -DVQPC_PHASE_TIMING build.
+extern "C" int vqpc_debug_pcg2d_phase_cycles(unsigned long long* out, int reset) {
+  if (!out) return VQPC_INVALID_ARGUMENT;
+#ifdef VQPC_PHASE_TIMING
+  if (cudaMemcpyFromSymbol(out, vqpc::g_pcg2d_phase, 4 * sizeof(unsigned long long)) != cudaSuccess)
+    return VQPC_CUDA_ERROR;
+  if (reset) {
+    const unsigned long long z[4] = {0, 0, 0, 0};
+    if (cudaMemcpyToSymbol(vqpc::g_pcg2d_phase, z, sizeof(z)) != cudaSuccess) return VQPC_CUDA_ERROR;
+  }
+#else
+  (void)reset;
+  for (int i = 0; i < 4; ++i) out[i] = 0;
+#endif
+  return VQPC_OK;
+}

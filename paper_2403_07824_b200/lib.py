@@ -72,6 +72,7 @@ def load():
             "vqpc_profile": (I, [VP, I]),
             "vqpc_profile_read": (I, [VP, VP, VP, I]),
             "vqpc_fp64_peak": (I, [I, C.POINTER(C.c_double)]),
+            "vqpc_debug_pcg2d_phase_cycles": (I, [C.POINTER(C.c_ulonglong), I]),
             "vqpc_counter_hash": (U64, [U64, U64, U64]),
             "vqpc_normal_quantile": (D, [D]),
         }
@@ -120,6 +121,13 @@ def fp64_peak(device=0):
     v = C.c_double()
     _check(load().vqpc_fp64_peak(device, C.byref(v)))
     return v.value
+
+
+def pcg2d_phase_cycles(reset=True):
+    """Cycles of the 2-D PCG phases (setup, sweeps, P1, P2); zeros unless built with -DVQPC_PHASE_TIMING."""
+    out = (C.c_ulonglong * 4)()
+    _check(load().vqpc_debug_pcg2d_phase_cycles(out, int(reset)))
+    return list(out)
 
 
 def counter_hash(seed, index, comp):
