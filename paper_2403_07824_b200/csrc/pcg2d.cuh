@@ -39,6 +39,7 @@
 namespace vqpc {
 
 constexpr int P2_T = 256;            // threads per CTA (one per grid row, r <= 257)
+constexpr int P2_FAC = 4;            // factor vectors per centroid: D, aW, aS, RN(1/D)
 constexpr int P2_MAXL = 2 * P2_T;    // max levels (2m - 1 <= 511)
 
 struct Grid2D {
@@ -213,8 +214,19 @@ __device__ unsigned long long g_pcg2d_phase[4];  // cycles: setup, sweeps, P1, P
 #define P2_TOC(i, v)
 #endif
 
+// Division by a pivot with its correctly rounded reciprocal R = RN(1/D):
+// q0 = x R, e = fma(-D, q0, x) (exact), q = fma(e, R, q0) equals RN(x / D)
+// (Markstein's theorem; normal range, which the IC(0) pivots and sweep values
+// are in). Three dependent FP64 ops instead of the division sequence on the
+// sweeps' per-level critical path; exact-mode tests check the bits.
+__device__ __forceinline__ double div_by_pivot(double x, double d, double r) {
+  const double q0 = __dmul_rn(x, r);
+  const double e = __fma_rn(-d, q0, x);
+  return __fma_rn(e, r, q0);
+}
+
 // ---- (e) IC(0) factor of every centroid matrix (one CTA per centroid) ---------
-// fac layout per centroid (3 n doubles, wavefront order): D, aW, aS of A_c.
+// fac layout per centroid (P2_FAC n doubles, wavefront order): D, aW, aS of A_c, RN(1/D).
 __global__ void __launch_bounds__(P2_T) factor2d_kernel(const double* kappa_c, int64_t ldk, int P, const Grid2D g,
                                                          double* fac, int* err) {
   __shared__ LevelTab tab;
@@ -223,9 +235,10 @@ __global__ void __launch_bounds__(P2_T) factor2d_kernel(const double* kappa_c, i
   const int p = blockIdx.x, t = threadIdx.x;
   if (p >= P) return;
   const double* kap = kappa_c + static_cast<size_t>(p) * ldk;
-  double* D = fac + static_cast<size_t>(p) * 3 * g.n;
+  double* D = fac + static_cast<size_t>(p) * P2_FAC * g.n;
   double* W = D + g.n;
   double* S = W + g.n;
+  double* R = S + g.n;
   for (int k = t; k <= P2_T; k += blockDim.x) dprev[0][k] = dprev[1][k] = 1.0;
   __syncthreads();
   bool ok = true;
@@ -244,6 +257,7 @@ __global__ void __launch_bounds__(P2_T) factor2d_kernel(const double* kappa_c, i
       D[a] = v;
       W[a] = rc.w;
       S[a] = rc.s;
+      R[a] = __drcp_rn(v);
     }
     __syncthreads();
   }
@@ -279,7 +293,7 @@ constexpr int P2_DEPTH = 6;
 #else
 constexpr int P2_DEPTH = P2_DEPTH_OVERRIDE;
 #endif  // cp.async prefetch ring depth (levels) for the IC(0) sweeps
-constexpr int P2_NOPS = 5;   // operands per node in the ring
+constexpr int P2_NOPS = 6;   // operands per node in the ring
 // Flat passes (P1, P2) stream the wavefront array in chunks of P2_T addresses:
 // each thread prefetches its own address of chunk k + P2_SD with cp.async into
 // a raw slot only it reads, and publishes the vector values its neighbours need
@@ -296,6 +310,9 @@ static_assert(P2_T == 256, "chunk indexing assumes 256-address chunks");
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8s(unsigned sa, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
@@ -343,11 +360,14 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
   constexpr int NW = P2_T / 32;
   extern __shared__ __align__(16) double dsm[];
   __shared__ double sbuf[2][P2_T + 2];  // previous level of the running sweep (index iy + 1)
+  __shared__ int2 lvl_dd[P2_MAXL];       // per level: a - a_W, a_E - a
   __shared__ double red[4][NW];
   __shared__ int64_t s_item;
   __shared__ double s_bval;
   const Grid2D g = prm.g;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int l = t; l < g.L; l += P2_T) lvl_dd[l] = make_int2(l > 0 ? wf_dw(l, g.m) : 0, l + 1 < g.L ? wf_de(l, g.m) : 0);
+  __syncthreads();
   const int n = g.n;
   double* base = prm.work + static_cast<size_t>(blockIdx.x) * P2_WORK * n;
   double* Ad = base;          // diagonal
@@ -386,9 +406,10 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
       continue;
     }
     const double* kap = prm.kappa + static_cast<size_t>(s) * prm.ldk;
-    const double* FD = prm.fac + static_cast<size_t>(label) * 3 * n;
+    const double* FD = prm.fac + static_cast<size_t>(label) * P2_FAC * n;
     const double* FW = FD + n;
     const double* FS = FW + n;
+    const double* FR = FS + n;
     int xc = 0, pc = 0;  // current ping-pong halves
 
     // ---- setup: assemble the sample's rows, x = 0, r = b ----------------------
@@ -430,80 +451,95 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
     };
     auto up = [&](int l) { return l < m - 1 ? l + 1 : 2 * m - 2 - l; };
     auto on = [&](int l) { return trow && static_cast<unsigned>(l - t) < static_cast<unsigned>(m); };
-    auto fwd_issue = [&](int l, int a) {
+    // ring slots as 32-bit shared addresses; slot counters instead of l % depth
+    const unsigned ring_sa = static_cast<unsigned>(__cvta_generic_to_shared(dsm)) + t * 8u;
+    constexpr unsigned OPB = P2_T * 8u, SLOTB = P2_NOPS * P2_T * 8u;
+    auto next_slot = [](int sl) { return sl + 1 == P2_DEPTH ? 0 : sl + 1; };
+    auto fwd_issue = [&](int l, int a, int sl) {
       if (on(l)) {
-        double* r0 = &ring[l % P2_DEPTH][0][t];
-        cp_async8(r0, Rv + a);
-        cp_async8(r0 + P2_T, FW + a);
-        cp_async8(r0 + 2 * P2_T, FS + a);
-        cp_async8(r0 + 3 * P2_T, FD + a);
+        const unsigned r0 = ring_sa + sl * SLOTB;
+        cp_async8s(r0, Rv + a);
+        cp_async8s(r0 + OPB, FW + a);
+        cp_async8s(r0 + 2 * OPB, FS + a);
+        cp_async8s(r0 + 3 * OPB, FD + a);
+        cp_async8s(r0 + 4 * OPB, FR + a);
       }
       cp_commit();
     };
-    auto bwd_issue = [&](int l, int a) {
+    auto bwd_issue = [&](int l, int a, int sl) {
       if (l >= 0 && on(l)) {
-        double* r0 = &ring[l % P2_DEPTH][0][t];
+        const unsigned r0 = ring_sa + sl * SLOTB;
         const int ae = a + up(l);  // (ix+1, iy) on level l+1; (ix, iy+1) is the next address
-        if (l - t < m - 1) cp_async8(r0, FW + ae);
-        if (t < m - 1) cp_async8(r0 + P2_T, FS + ae + 1);
-        cp_async8(r0 + 2 * P2_T, FD + a);
-        cp_async8(r0 + 3 * P2_T, Y + a);
-        cp_async8(r0 + 4 * P2_T, Rv + a);
+        if (l - t < m - 1) cp_async8s(r0, FW + ae);
+        if (t < m - 1) cp_async8s(r0 + OPB, FS + ae + 1);
+        cp_async8s(r0 + 2 * OPB, FD + a);
+        cp_async8s(r0 + 3 * OPB, Y + a);
+        cp_async8s(r0 + 4 * OPB, Rv + a);
+        cp_async8s(r0 + 5 * OPB, FR + a);
       }
       cp_commit();
     };
     auto sweeps = [&]() -> double {
-      // forward (D + L) y = r, ascending levels
+      // forward (D + L) y = r, ascending levels; level l lives in ring slot l % depth
       __syncthreads();
       int ai = lin(0), ac = ai;  // issue / compute cursors
+      int si = 0, sc = 0;        // issue / compute slots
       for (int l = 0; l < P2_DEPTH - 1; ++l) {
-        fwd_issue(l, ai);
+        fwd_issue(l, ai, si);
         ai += up(l);
+        si = next_slot(si);
       }
       for (int l = 0; l < g.L; ++l) {
-        fwd_issue(l + P2_DEPTH - 1, ai);  // slot of level l-1, already consumed
+        fwd_issue(l + P2_DEPTH - 1, ai, si);  // slot of level l-1, already consumed
         ai += up(l + P2_DEPTH - 1);
+        si = next_slot(si);
         cp_wait<P2_DEPTH - 1>();
         const int cur = l & 1, prv = cur ^ 1;
         if (on(l)) {
-          const double* op = &ring[l % P2_DEPTH][0][t];
+          const double* op = &ring[sc][0][t];
           double v = op[0];
           if (l - t > 0) v = __dsub_rn(v, __dmul_rn(op[P2_T], sbuf[prv][t + 1]));
           if (t > 0) v = __dsub_rn(v, __dmul_rn(op[2 * P2_T], sbuf[prv][t]));
-          v = __ddiv_rn(v, op[3 * P2_T]);
+          v = div_by_pivot(v, op[3 * P2_T], op[4 * P2_T]);
           Y[ac] = v;
           sbuf[cur][t + 1] = v;
         }
         ac += up(l);
+        sc = next_slot(sc);
         __syncthreads();
       }
       cp_wait<0>();
       __syncthreads();  // Y complete before the backward prefetch reads it
-      // backward (D + L^T) z = D y, descending levels: z_i = y_i - (aE z_E + aN z_N) / D_i
+      // backward (D + L^T) z = D y, descending levels: z_i = y_i - (aE z_E + aN z_N) / D_i;
+      // level l lives in ring slot (L - 1 - l) % depth
       double rz_part = 0.0;
       ai = lin(g.L - 1);
       ac = ai;
+      si = sc = 0;
       for (int l = g.L - 1; l > g.L - P2_DEPTH; --l) {
-        bwd_issue(l, ai);
+        bwd_issue(l, ai, si);
         ai -= up(l - 1);
+        si = next_slot(si);
       }
       for (int l = g.L - 1; l >= 0; --l) {
-        bwd_issue(l - (P2_DEPTH - 1), ai);
+        bwd_issue(l - (P2_DEPTH - 1), ai, si);
         ai -= up(l - P2_DEPTH);
+        si = next_slot(si);
         cp_wait<P2_DEPTH - 1>();
         const int cur = l & 1, prv = cur ^ 1;
         if (on(l)) {
-          const double* op = &ring[l % P2_DEPTH][0][t];
+          const double* op = &ring[sc][0][t];
           double acc = 0.0;
           if (l - t < m - 1) acc = __dadd_rn(acc, __dmul_rn(op[0], sbuf[prv][t + 1]));
           if (t < m - 1) acc = __dadd_rn(acc, __dmul_rn(op[P2_T], sbuf[prv][t + 2]));
-          const double z = __dsub_rn(op[3 * P2_T], __ddiv_rn(acc, op[2 * P2_T]));
+          const double z = __dsub_rn(op[3 * P2_T], div_by_pivot(acc, op[2 * P2_T], op[5 * P2_T]));
           Z[ac] = z;
           sbuf[cur][t + 1] = z;
           rz_part = fma(op[4 * P2_T], z, rz_part);
           if (exact) Prod[t * m + (l - t)] = __dmul_rn(op[4 * P2_T], z);
         }
         ac -= up(l - 1);
+        sc = next_slot(sc);
         __syncthreads();
       }
       cp_wait<0>();
@@ -530,8 +566,9 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
         double* raw = dsm;                                   // [P2_RSLOT][P2_RAW][P2_T]
         double* xch = dsm + P2_RSLOT * P2_RAW * P2_T;        // [P2_XCH][4][P2_T]
         int* rawi = reinterpret_cast<int*>(xch + 4 * P2_XCH * P2_T);  // [P2_RSLOT][P2_T]
-        auto RAW = [&](int k, int v) -> double* { return raw + ((k % P2_RSLOT) * P2_RAW + v) * P2_T + t; };
-        auto XCH = [&](int x, int q) -> double& { return xch[(x * 4 + ((q >> 8) & 3)) * P2_T + (q & (P2_T - 1))]; };
+        auto RAW = [&](int k, int v) -> double* { return raw + ((static_cast<unsigned>(k) % P2_RSLOT) * P2_RAW + v) * P2_T + t; };
+        // chunk slot (q >> 8) & 3, column q & 255: together q & 1023
+        auto XCH = [&](int x, int q) -> double& { return xch[x * 4 * P2_T + (q & (4 * P2_T - 1))]; };
         auto flat_issue = [&](int k, const double* v0, const double* v1, const double* v2) {
           const int a = k * P2_T + t;
           if (k < NC && a < n) {
@@ -541,7 +578,7 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
             cp_async8(RAW(k, 3), As + a);
             cp_async8(RAW(k, 4), Aw + a);
             cp_async8(RAW(k, 5), Ad + a);
-            cp_async4(rawi + (k % P2_RSLOT) * P2_T + t, prm.gmap + a);
+            cp_async4(rawi + (static_cast<unsigned>(k) % P2_RSLOT) * P2_T + t, prm.gmap + a);
           }
           cp_commit();
         };
@@ -550,7 +587,8 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
         auto nbrs = [&](int a, int lv) {
           const int l = lv & 0xffff, iy = lv >> 16, ix = l - iy;
           Nb b;
-          const int dw = wf_dw(l, g.m), de = wf_de(l, g.m);
+          const int2 dd = lvl_dd[l];
+          const int dw = dd.x, de = dd.y;
           b.w = ix > 0 ? a - dw : -1;
           b.s = iy > 0 ? a - dw - 1 : -1;
           b.e = ix < g.m - 1 ? a + de : -1;
@@ -577,7 +615,7 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
                 cs = *RAW(k, 3);
                 cw = *RAW(k, 4);
                 cd = *RAW(k, 5);
-                clv = rawi[(k % P2_RSLOT) * P2_T + t];
+                clv = rawi[(static_cast<unsigned>(k) % P2_RSLOT) * P2_T + t];
                 XCH(0, a) = pcv;
                 XCH(2, a) = cw;
                 XCH(3, a) = cs;
@@ -630,7 +668,7 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
                 cs = *RAW(k, 3);
                 cw = *RAW(k, 4);
                 cd = *RAW(k, 5);
-                clv = rawi[(k % P2_RSLOT) * P2_T + t];
+                clv = rawi[(static_cast<unsigned>(k) % P2_RSLOT) * P2_T + t];
                 XCH(0, a) = pvv;
                 XCH(1, a) = xn;
                 XCH(2, a) = cw;
@@ -709,7 +747,7 @@ __global__ void __launch_bounds__(P2_T) precond2d_apply_kernel(const double* fac
   __shared__ double sbuf[2][P2_T + 2];
   build_levels(tab, g);
   const int t = threadIdx.x, n = g.n;
-  const double* FD = fac + static_cast<size_t>(p) * 3 * n;
+  const double* FD = fac + static_cast<size_t>(p) * P2_FAC * n;
   const double* FW = FD + n;
   const double* FS = FW + n;
   double* Y = ws;

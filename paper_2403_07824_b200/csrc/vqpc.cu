@@ -633,7 +633,7 @@ int vqpc_factor_centroids(vqpc_ctx* c) {
     c->err.ensure(1);
     CK(cudaMemsetAsync(c->err.p, 0, sizeof(int), c->stream));
     if (pb.dim == 2) {
-      c->fac2.ensure(static_cast<size_t>(P) * 3 * c->n);
+      c->fac2.ensure(static_cast<size_t>(P) * P2_FAC * c->n);
       Timed tm(c, VQPC_K_OTHER);
       factor2d_kernel<<<P, P2_T, 0, c->stream>>>(c->kappa_c.p, ldk, P, c->g2, c->fac2.p, c->err.p);
       launch_check(c);
