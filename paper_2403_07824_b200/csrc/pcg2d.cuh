@@ -315,6 +315,25 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async8s(unsigned sa, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
 }
+// same with an L2 eviction-priority policy (createpolicy): the centroid factors
+// are shared by every CTA of a bucket and should stay in L2 (evict_last) while
+// the per-sample vectors stream through it (evict_first)
+__device__ __forceinline__ unsigned long long l2_policy_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long l2_policy_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void cp_async8h(unsigned sa, const void* gmem, unsigned long long pol) {
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void cp_async8p(void* smem, const void* gmem, unsigned long long pol) {
+  cp_async8h(static_cast<unsigned>(__cvta_generic_to_shared(smem)), gmem, pol);
+}
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
@@ -356,6 +375,9 @@ __device__ __forceinline__ double serial_sum2d(const double* prod, int n, double
   return v;
 }
 
+// MC > 0 compiles the kernel for a fixed interior size m = MC (BASELINE C4: 255):
+// every vector offset j*n becomes an immediate and the level arithmetic folds.
+template <int MC>
 __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
   constexpr int NW = P2_T / 32;
   extern __shared__ __align__(16) double dsm[];
@@ -364,7 +386,12 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
   __shared__ double red[4][NW];
   __shared__ int64_t s_item;
   __shared__ double s_bval;
-  const Grid2D g = prm.g;
+  Grid2D g = prm.g;
+  if constexpr (MC > 0) {
+    g.m = MC;
+    g.n = MC * MC;
+    g.L = 2 * MC - 1;
+  }
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   for (int l = t; l < g.L; l += P2_T) lvl_dd[l] = make_int2(l > 0 ? wf_dw(l, g.m) : 0, l + 1 < g.L ? wf_de(l, g.m) : 0);
   __syncthreads();
@@ -453,16 +480,17 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
     auto on = [&](int l) { return trow && static_cast<unsigned>(l - t) < static_cast<unsigned>(m); };
     // ring slots as 32-bit shared addresses; slot counters instead of l % depth
     const unsigned ring_sa = static_cast<unsigned>(__cvta_generic_to_shared(dsm)) + t * 8u;
+    const unsigned long long pol_fac = l2_policy_last();
     constexpr unsigned OPB = P2_T * 8u, SLOTB = P2_NOPS * P2_T * 8u;
     auto next_slot = [](int sl) { return sl + 1 == P2_DEPTH ? 0 : sl + 1; };
     auto fwd_issue = [&](int l, int a, int sl) {
       if (on(l)) {
         const unsigned r0 = ring_sa + sl * SLOTB;
         cp_async8s(r0, Rv + a);
-        cp_async8s(r0 + OPB, FW + a);
-        cp_async8s(r0 + 2 * OPB, FS + a);
-        cp_async8s(r0 + 3 * OPB, FD + a);
-        cp_async8s(r0 + 4 * OPB, FR + a);
+        cp_async8h(r0 + OPB, FW + a, pol_fac);
+        cp_async8h(r0 + 2 * OPB, FS + a, pol_fac);
+        cp_async8h(r0 + 3 * OPB, FD + a, pol_fac);
+        cp_async8h(r0 + 4 * OPB, FR + a, pol_fac);
       }
       cp_commit();
     };
@@ -470,12 +498,12 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
       if (l >= 0 && on(l)) {
         const unsigned r0 = ring_sa + sl * SLOTB;
         const int ae = a + up(l);  // (ix+1, iy) on level l+1; (ix, iy+1) is the next address
-        if (l - t < m - 1) cp_async8s(r0, FW + ae);
-        if (t < m - 1) cp_async8s(r0 + OPB, FS + ae + 1);
-        cp_async8s(r0 + 2 * OPB, FD + a);
+        if (l - t < m - 1) cp_async8h(r0, FW + ae, pol_fac);
+        if (t < m - 1) cp_async8h(r0 + OPB, FS + ae + 1, pol_fac);
+        cp_async8h(r0 + 2 * OPB, FD + a, pol_fac);
         cp_async8s(r0 + 3 * OPB, Y + a);
         cp_async8s(r0 + 4 * OPB, Rv + a);
-        cp_async8s(r0 + 5 * OPB, FR + a);
+        cp_async8h(r0 + 5 * OPB, FR + a, pol_fac);
       }
       cp_commit();
     };
@@ -569,15 +597,16 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
         auto RAW = [&](int k, int v) -> double* { return raw + ((static_cast<unsigned>(k) % P2_RSLOT) * P2_RAW + v) * P2_T + t; };
         // chunk slot (q >> 8) & 3, column q & 255: together q & 1023
         auto XCH = [&](int x, int q) -> double& { return xch[x * 4 * P2_T + (q & (4 * P2_T - 1))]; };
+        const unsigned long long pol_str = l2_policy_first();
         auto flat_issue = [&](int k, const double* v0, const double* v1, const double* v2) {
           const int a = k * P2_T + t;
           if (k < NC && a < n) {
-            if (v0) cp_async8(RAW(k, 0), v0 + a);
-            if (v1) cp_async8(RAW(k, 1), v1 + a);
-            if (v2) cp_async8(RAW(k, 2), v2 + a);
-            cp_async8(RAW(k, 3), As + a);
-            cp_async8(RAW(k, 4), Aw + a);
-            cp_async8(RAW(k, 5), Ad + a);
+            if (v0) cp_async8p(RAW(k, 0), v0 + a, pol_str);
+            if (v1) cp_async8p(RAW(k, 1), v1 + a, pol_str);
+            if (v2) cp_async8p(RAW(k, 2), v2 + a, pol_str);
+            cp_async8p(RAW(k, 3), As + a, pol_str);
+            cp_async8p(RAW(k, 4), Aw + a, pol_str);
+            cp_async8p(RAW(k, 5), Ad + a, pol_str);
             cp_async4(rawi + (static_cast<unsigned>(k) % P2_RSLOT) * P2_T + t, prm.gmap + a);
           }
           cp_commit();

@@ -259,8 +259,10 @@ void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d
                const int32_t* d_labels, int64_t B, int64_t out_base, double eps, int max_iter, const int32_t* d_mia,
                int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x, int64_t solve_limit) {
   int per_sm = 0;
-  CK(cudaFuncSetAttribute(pcg2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P2_DSMEM)));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg2d_kernel, P2_T, P2_DSMEM));
+  // C4's mesh (m = 255) has a specialised instantiation; other sizes take the generic one
+  void (*kern)(const Pcg2dParams) = c->g2.m == 255 ? pcg2d_kernel<255> : pcg2d_kernel<0>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P2_DSMEM)));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P2_T, P2_DSMEM));
   if (per_sm < 1) throw ApiError{VQPC_CUDA_ERROR, "pcg2d kernel does not fit on an SM"};
   const int64_t blocks = std::min<int64_t>(B, static_cast<int64_t>(per_sm) * c->sm_count);
   c->work2.ensure(static_cast<size_t>(blocks) * P2_WORK * c->n);
@@ -294,7 +296,7 @@ void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d
   }
   prm.gmap = c->gmap.p;
   Timed tm(c, VQPC_K_PCG);
-  pcg2d_kernel<<<static_cast<unsigned>(blocks), P2_T, P2_DSMEM, c->stream>>>(prm);
+  kern<<<static_cast<unsigned>(blocks), P2_T, P2_DSMEM, c->stream>>>(prm);
   launch_check(c);
 }
 
