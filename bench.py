@@ -62,12 +62,26 @@ def parse():
 
 
 def workload(cfg, B, K):
-    return {"workload": f"{cfg['name']}: 1-D P1 FEM, {cfg['mesh_resolution'] - 1} unknowns, "
-                        f"{B} samples/GPU, KL {K} modes (n_KL={cfg['n_kl']}), {cfg['quantizer']['method']} "
-                        f"d={cfg['m']} P={cfg['quantizer']['P']}, tridiagonal-Cholesky PCG rtol {cfg['eps']:g}",
-            "samples_per_gpu": B, "unknowns": cfg["mesh_resolution"] - 1, "n_kl": K, "d": cfg["m"],
-            "P": cfg["quantizer"]["P"], "eps": cfg["eps"],
-            "l2": "inputs larger than L2 (kappa %.1f GB written and read per step)" % (B * cfg["mesh_resolution"] * 8 / 1e9)}
+    n = (cfg["mesh_resolution"] - 1) ** cfg["dim"]
+    q = cfg["quantizer"]
+    sub = cfg.get("solve_subset")
+    if cfg["dim"] == 1:
+        model = f"1-D P1 FEM, {n} unknowns"
+        pc = "tridiagonal-Cholesky"
+        kap = B * cfg["mesh_resolution"] * 8
+    else:
+        r = cfg["mesh_resolution"]
+        model = f"2-D P1 FEM on a {r}x{r} right-triangle mesh, {n} unknowns"
+        pc = "IC(0)"
+        kap = B * (r + 1) ** 2 * 8
+    solve = f", PCG on the first {sub} samples" if sub else ""
+    chunk = f", chunks of {cfg['chunk']}" if cfg.get("chunk") else ""
+    return {"workload": f"{cfg['name']}: {model}, {B} samples/GPU{chunk}, KL {K} modes (n_KL={cfg['n_kl']}), "
+                        f"{q['method']} d={cfg['m']} P={q['P']}, {pc} PCG rtol {cfg['eps']:g}{solve}",
+            "samples_per_gpu": B, "unknowns": n, "n_kl": K, "d": cfg["m"], "P": q["P"], "eps": cfg["eps"],
+            "solve_subset": sub,
+            "l2": "inputs larger than L2 (kappa %.1f GB written and read per step)" % (kap / 1e9)
+            if kap > 126e6 else "per-step working set %.0f MB (kappa) + per-CTA PCG vectors" % (kap / 1e6)}
 
 
 class Clocks:
@@ -117,6 +131,13 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_sample_size(cfg):
+    """Bounded CPU sample (10-30 s of oracle work on the box's host cores)."""
+    if cfg["dim"] == 2:
+        return 32  # ~1.5-2 s per C4 sample per core
+    return 512 if cfg["mesh_resolution"] >= 4096 else 2048
+
+
 def cpu_baseline(cfg, arts, n_cpu, index0=0):
     """The CPU oracle's run_campaign_with on a bounded sample (all host threads)."""
     import oracle
@@ -146,7 +167,7 @@ def run_reference(args, rank, world):
     oracle.build()
     arts = campaign.prepare_campaign(cfg, kmeans_fn=oracle.kmeans, draw_fn=oracle.draw_standard_normal)
     K = arts["basis"]["eigenvalues"].size
-    n_step = args.cpu_samples or (256 if cfg["mesh_resolution"] >= 4096 else 1024)
+    n_step = args.cpu_samples or max(cpu_sample_size(cfg) // 2, 16)
     times = []
     last = None
     for s in range(args.warmup + args.steps):
@@ -166,6 +187,68 @@ def run_reference(args, rank, world):
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "mean_pcg_iters": last["mean_pcg_iters"]}
     print(json.dumps(line), flush=True)
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+def roofline(cfg, prof, total_iters, B, steps, device):
+    """Roofline of the step's dominant kernel (largest event-timed share).
+
+    Algorithmic work per unit is SURVEY §8(d)'s: 1-D PCG 31 n flops per
+    iteration (fp64 pipe); 2-D PCG 8 (2 N_nodes + 14 n) bytes per iteration
+    (HBM); realise 2 N K flops per sample (fp64 DMMA); assign 3 P d exact fp64
+    operations per sample. The fp64 peak is measured on this device by
+    vqpc_fp64_peak (DFMA probe; MEASURED_PEAKS.json has no fp64 entry), the HBM
+    peak is MEASURED_PEAKS.json's copy bandwidth."""
+    from paper_2403_07824_b200 import lib
+    kind = max(("pcg", "realise", "assign"), key=lambda k: prof[k]["ms"])
+    k = prof[kind]
+    ms = k["ms"] / max(k["launches"], 1)
+    lps = max(k["launches"] // steps, 1)  # launches per step
+    r = cfg["mesh_resolution"]
+    n = (r - 1) ** cfg["dim"]
+    npts = r if cfg["dim"] == 1 else (r + 1) ** 2
+    K, P, d = cfg["n_kl"], cfg["quantizer"]["P"], cfg["m"]
+    traffic = None
+    summ = os.path.join(ROOT, "profiles", "pcg_ncu_summary.json")
+    if os.path.exists(summ):
+        try:
+            traffic = json.load(open(summ)).get(cfg["name"], {}).get("dram_bytes_per_launch")
+        except (OSError, ValueError, AttributeError):
+            traffic = None
+    if kind == "pcg" and cfg["dim"] == 2:
+        work = 8.0 * (2 * npts + 14 * n) * total_iters / lps
+        peak = measured_peaks().get("hbm_gbs")
+        achieved = work / (ms / 1e3) / 1e9
+        return {"kernel": "pcg2d", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if peak else None, "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, this pool's B200s)",
+                "algorithmic": "8 (2 N_nodes + 14 n) bytes per PCG iteration x sum of J over the batch (SURVEY 8d)",
+                "ms_per_launch": ms}
+    if kind == "pcg":
+        work = 31.0 * n * total_iters / lps
+        what = "31 n flops per PCG iteration x sum of J over the batch (SURVEY 8d)"
+        name = "pcg1d"
+    elif kind == "realise":
+        work = 2.0 * npts * K * B / lps
+        what = "2 N K flops per sample (SURVEY 8d)"
+        name = "realise"
+    else:
+        work = 3.0 * P * d * B / lps
+        what = "3 P d exact fp64 ops per sample (SURVEY 8d)"
+        name = "assign"
+    peak = lib.fp64_peak(device)
+    achieved = work / (ms / 1e3) / 1e12
+    return {"kernel": name, "bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak if peak else None, "traffic": traffic,
+            "peak_source": "measured on this device: vqpc_fp64_peak DFMA-throughput probe "
+                           "(MEASURED_PEAKS.json has no fp64 entry)",
+            "algorithmic": what, "ms_per_launch": ms}
 
 
 def run_ours(args, rank, world, local_rank):
@@ -197,13 +280,15 @@ def run_ours(args, rank, world, local_rank):
     d_st = torch.empty(B, dtype=torch.uint8, device=dev)
     d_stats = torch.empty(4 * P + 4, dtype=torch.int64, device=dev)
     stream = torch.cuda.Stream(device=dev)
+    # C5: realise + assign every sample, PCG on the first solve_subset of the master stream
+    solve_limit = max(0, min(B, cfg["solve_subset"] - rank * B)) if cfg.get("solve_subset") else -1
     ctx = campaign.make_context(cfg, arts, device=local_rank)
     ctx.set_stream(stream.cuda_stream)
 
     def step():
         ctx.run_campaign_device(d_xi.data_ptr(), B, K, cfg["eps"], d_lab.data_ptr(), d_it.data_ptr(),
                                 d_rel.data_ptr(), d_st.data_ptr(), d_stats.data_ptr(), d_stats.data_ptr() + 8 * 4 * P,
-                                chunk=cfg.get("chunk", 0))
+                                chunk=cfg.get("chunk", 0), solve_limit=solve_limit)
         if dist:
             with torch.cuda.stream(stream):
                 dist.all_reduce(d_stats)  # per-centroid n_p / sum_J / converged stats (driver.cpp:241-258)
@@ -243,20 +328,7 @@ def run_ours(args, rank, world, local_rank):
     conv = st == 0
     n = cfg["mesh_resolution"] - 1
 
-    # roofline of the dominant kernel (pcg): algorithmic fp64 flops / event time
-    pcg = prof["pcg"]
-    pcg_ms = pcg["ms"] / max(pcg["launches"], 1)
-    launches_per_step = max(pcg["launches"] // args.steps, 1)
-    flops_per_launch = FLOPS_PER_ROW_ITER * n * total_iters / launches_per_step
-    achieved = flops_per_launch / (pcg_ms / 1e3) / 1e12
-    peak = lib.fp64_peak(local_rank)
-    traffic = None
-    summ = os.path.join(ROOT, "profiles", "pcg_ncu_summary.json")
-    if os.path.exists(summ):
-        try:
-            traffic = json.load(open(summ)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    roof = roofline(cfg, prof, total_iters, B, args.steps, local_rank)
     step_ms = ms_max / args.steps
     kernels = {k: {"ms_per_step": v["ms"] / args.steps, "share": (v["ms"] / args.steps) / step_ms if step_ms else 0,
                    "launches": v["launches"]} for k, v in prof.items()}
@@ -266,7 +338,7 @@ def run_ours(args, rank, world, local_rank):
     for s in range(args.steps + 1):
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        res = ctx.run_campaign(xi_pin.numpy(), cfg["eps"], chunk=cfg.get("chunk", 0))
+        res = ctx.run_campaign(xi_pin.numpy(), cfg["eps"], chunk=cfg.get("chunk", 0), solve_limit=solve_limit)
         e2e_times.append(time.perf_counter() - t0)
     e2e_t = float(np.sum(e2e_times[1:]))  # first call warms the host-side buffers
     e2e_val = world * B * args.steps / e2e_t
@@ -280,7 +352,7 @@ def run_ours(args, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        n_cpu = args.cpu_samples or (512 if cfg["mesh_resolution"] >= 4096 else 2048)
+        n_cpu = args.cpu_samples or cpu_sample_size(cfg)
         cpu = cpu_baseline(cfg, arts, n_cpu)
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
@@ -293,12 +365,7 @@ def run_ours(args, rank, world, local_rank):
                 "mean_pcg_iters": float(it[conv].mean()) if conv.any() else 0.0,
                 "status_counts": {lib.STATUS[k]: int((st == k).sum()) for k in np.unique(st)},
                 "total_pcg_iterations_per_gpu_step": total_iters,
-                "roofline": {"kernel": "pcg1d", "bound": "fp64", "achieved": achieved, "peak": peak,
-                             "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": traffic,
-                             "peak_source": "measured on this device: vqpc_fp64_peak DFMA-throughput probe "
-                                            "(MEASURED_PEAKS.json has no fp64 entry)",
-                             "algorithmic": f"{FLOPS_PER_ROW_ITER} n flops per PCG iteration x sum of J over the batch",
-                             "ms_per_launch": pcg_ms},
+                "roofline": roof,
                 "kernels": kernels,
                 "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                 "gpu_launches": int(launches),
