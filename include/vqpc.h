@@ -182,6 +182,9 @@ int vqpc_fp64_peak(int device, double* tflops);
  * summed over CTAs (all zero unless the library was built with
  * -DVQPC_PHASE_TIMING). */
 int vqpc_debug_pcg2d_phase_cycles(unsigned long long* out4, int reset);
+/* Same for the 1-D PCG: cycles between its four per-iteration barriers (CTA
+ * thread 0 of every sample, summed). */
+int vqpc_debug_pcg1d_phase_cycles(unsigned long long* out4, int reset);
 
 /* ---- quantizer construction on the host with device assignment sweeps ----
  * kmeans = minmax seeding + Lloyd (quantizer.cpp:181-357), bit-identical to

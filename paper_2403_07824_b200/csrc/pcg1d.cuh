@@ -34,8 +34,9 @@
 //   alpha; x += alpha p; r -= alpha Ap
 //   r_true = b - A x; rr = |r_true|^2   (rides barrier 2)
 //   sweep 1                             -> barrier 2 (warp aggregates + rr)
-//   rel = sqrt(rr)/|b|; record; rel < eps -> converged
+//   rel = sqrt(rr)/|b|
 //   sweep 2                             -> barrier 3 (warp aggregates)
+//   record; rel < eps -> converged (the exit waits for sweep 2: off the critical path)
 //   rz' = r.z                            -> barrier 4 (reduction + z halos)
 //   beta = rz'/rz; p = z + beta p
 // Halo values of x and p are never exchanged: each thread updates its copy of
@@ -87,7 +88,26 @@ struct Pcg1dParams {
   double* rel;
   uint8_t* status;
   double* x_out;              // nullable, (global sample) x n
+  unsigned long long* t_span;  // nullable diagnostics: per CTA {start, end} %globaltimer (ns)
 };
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  return v;
+}
+
+#ifdef VQPC_PHASE_TIMING
+__device__ unsigned long long g_pcg1d_phase[4];  // cycles from each barrier to the next (thread 0)
+#define P1D_MARK(i)                                                                         \
+  if (tid == 0 && rank == 0) {                                                              \
+    const long long now_ = clock64();                                                       \
+    if (ph_last >= 0) atomicAdd(&g_pcg1d_phase[i], static_cast<unsigned long long>(now_ - ph_last)); \
+    ph_last = now_;                                                                         \
+  }
+#else
+#define P1D_MARK(i)
+#endif
 
 template <int R, int T, int CL>
 struct Pcg1dShared {
@@ -207,7 +227,11 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
   const double2* fact = S.fac + tid;   // fact[i*T]
   const double* c_halo = tid + 1 < T ? &S.cd[tid + 1].x : &S.cs_end;  // c_{j0+R}
 
+  if (prm.t_span && tid == 0) prm.t_span[2 * blockIdx.x] = globaltimer_ns();
   int cur_label = -1;
+#ifdef VQPC_PHASE_TIMING
+  long long ph_last = -1;
+#endif
   double nc[R];         // n_j of own rows
   double n_left = 0.0;  // n_{j0-1}
 
@@ -329,6 +353,7 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
           publish(S.red[1], gwarp, rrw);
         }
         bar();  // barrier 2
+        P1D_MARK(1);  // alpha, x/r update, true residual, sweep 1
         double vw = 0.0;
 #pragma unroll
         for (int w2 = NWT - 1; w2 > 0; --w2)
@@ -352,16 +377,9 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
 #pragma unroll
         for (int i = 0; i < R; ++i) wz[i] *= fact[i * T].y;
       }
-      if (j > 0) {
-        const double rr = tree_sum<NWT>(S.red[1]);
-        const double rel = sqrt(rr) / norm_b;
-        J = j;
-        rel_rec = rel;
-        if (rel < prm.eps) {
-          st = VQPC_S_CONVERGED;
-          break;
-        }
-      }
+      // the relative true residual decides convergence; its sqrt and division
+      // overlap sweep 2, and the (warp-uniform) exit is taken after it
+      const double rel = j > 0 ? sqrt(tree_sum<NWT>(S.red[1])) / norm_b : 0.0;
       // ================= sweep 2 (ascending): barrier 3 =====================
       {
         double v[4];
@@ -379,6 +397,7 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
         for (int k = 0; k < 5; ++k) W = fma(levt[(6 + k) * T], shfl_up(W, 1 << k), W);
         if (lane == 31) publish(&S.f2[0].x, 2 * gwarp + 1, W);
         bar();  // barrier 3
+        P1D_MARK(2);  // fold + fix-up of sweep 1, sweep 2
         double vw = 0.0;
 #pragma unroll
         for (int w2 = 0; w2 < NWT - 1; ++w2)
@@ -401,6 +420,14 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) wz[q * Q + i] = fma(-nc[q * Q + i - 1], wz[q * Q + i - 1], wz[q * Q + i]);
       }
+      if (j > 0) {
+        J = j;
+        rel_rec = rel;
+        if (rel < prm.eps) {
+          st = VQPC_S_CONVERGED;
+          break;
+        }
+      }
       // ================= rz (+|b|^2 at setup), z halos: barrier 4 ===========
       {
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
@@ -415,6 +442,7 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
         S.zf[tid] = wz[0];
         S.zl[tid] = wz[R - 1];
         bar();  // barrier 4
+        P1D_MARK(3);  // fold + fix-up of sweep 2, r.z
       }
       const double rz_next = tree_sum<NWT>(S.red[2]);
       // z halos; across the CTA boundary they are read from the peer (DSMEM)
@@ -481,6 +509,7 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
         const double a = warp_allsum((acc[0] + acc[1]) + (acc[2] + acc[3]));
         if (lane == 0) publish(S.red[0], gwarp, a);
         bar();  // barrier 1
+        P1D_MARK(0);  // p update, A p, p.Ap
       }
       const double pAp = tree_sum<NWT>(S.red[0]);
       if (!(pAp > 0.0)) {
@@ -512,6 +541,7 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
         if (j0 + i < n) xo[j0 + i] = x[i];
     }
   }
+  if (prm.t_span && tid == 0) prm.t_span[2 * blockIdx.x + 1] = globaltimer_ns();
   if constexpr (CL == 2) cg::this_cluster().sync();  // no CTA exits while its peer may read its smem
 }
 

@@ -361,9 +361,36 @@ void run_pcg(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d_k
   if (groups < 1) throw ApiError{VQPC_CUDA_ERROR, "pcg kernel does not fit on the device"};
   groups = std::min<int64_t>(B, groups);
   cfg.gridDim = dim3(static_cast<unsigned>(groups * v->CL));
-  Timed tm(c, VQPC_K_PCG);
-  CK(cudaLaunchKernelEx(&cfg, v->fn, prm));
-  launch_check(c);
+  // diagnostics (VQPC_TAIL=1): per-CTA busy span, to size the work-queue tail
+  static const bool tail = getenv("VQPC_TAIL") != nullptr;
+  unsigned long long* d_span = nullptr;
+  const unsigned nblk = cfg.gridDim.x;
+  if (tail) {
+    CK(cudaMallocAsync(&d_span, 2 * sizeof(unsigned long long) * nblk, c->stream));
+    prm.t_span = d_span;
+  }
+  {
+    Timed tm(c, VQPC_K_PCG);
+    CK(cudaLaunchKernelEx(&cfg, v->fn, prm));
+    launch_check(c);
+  }
+  if (tail) {
+    std::vector<unsigned long long> h(2 * nblk);
+    CK(cudaMemcpyAsync(h.data(), d_span, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaFreeAsync(d_span, c->stream));
+    unsigned long long t0 = ~0ull, t1 = 0;
+    std::vector<double> ends;
+    for (unsigned b = 0; b < nblk; ++b) {
+      t0 = std::min(t0, h[2 * b]);
+      t1 = std::max(t1, h[2 * b + 1]);
+    }
+    for (unsigned b = 0; b < nblk; ++b) ends.push_back(1e-6 * static_cast<double>(h[2 * b + 1] - t0));
+    std::sort(ends.begin(), ends.end());
+    fprintf(stderr, "[vqpc tail] pcg1d B=%lld ctas=%u span %.3f ms; CTA end ms: min %.3f p10 %.3f median %.3f p90 %.3f max %.3f\n",
+            static_cast<long long>(B), nblk, 1e-6 * static_cast<double>(t1 - t0), ends.front(), ends[nblk / 10],
+            ends[nblk / 2], ends[9 * nblk / 10], ends.back());
+  }
 }
 
 __global__ void stats_kernel(const int32_t* labels, const int32_t* iters, const uint8_t* status, int64_t B, int P,
@@ -865,6 +892,22 @@ int vqpc_run_campaign(vqpc_ctx* c, const double* xi, int64_t B, int ld, double e
 
 // Diagnostics: per-phase cycles of the 2-D PCG (setup, sweeps, P1, P2), summed
 // over CTAs by thread 0; nonzero only in a -DVQPC_PHASE_TIMING build.
+extern "C" int vqpc_debug_pcg1d_phase_cycles(unsigned long long* out, int reset) {
+  if (!out) return VQPC_INVALID_ARGUMENT;
+#ifdef VQPC_PHASE_TIMING
+  if (cudaMemcpyFromSymbol(out, vqpc::g_pcg1d_phase, 4 * sizeof(unsigned long long)) != cudaSuccess)
+    return VQPC_CUDA_ERROR;
+  if (reset) {
+    const unsigned long long z[4] = {0, 0, 0, 0};
+    if (cudaMemcpyToSymbol(vqpc::g_pcg1d_phase, z, sizeof(z)) != cudaSuccess) return VQPC_CUDA_ERROR;
+  }
+#else
+  (void)reset;
+  for (int i = 0; i < 4; ++i) out[i] = 0;
+#endif
+  return VQPC_OK;
+}
+
 extern "C" int vqpc_debug_pcg2d_phase_cycles(unsigned long long* out, int reset) {
   if (!out) return VQPC_INVALID_ARGUMENT;
 #ifdef VQPC_PHASE_TIMING

@@ -73,6 +73,7 @@ def load():
             "vqpc_profile_read": (I, [VP, VP, VP, I]),
             "vqpc_fp64_peak": (I, [I, C.POINTER(C.c_double)]),
             "vqpc_debug_pcg2d_phase_cycles": (I, [C.POINTER(C.c_ulonglong), I]),
+            "vqpc_debug_pcg1d_phase_cycles": (I, [C.POINTER(C.c_ulonglong), I]),
             "vqpc_counter_hash": (U64, [U64, U64, U64]),
             "vqpc_normal_quantile": (D, [D]),
         }
@@ -127,6 +128,14 @@ def pcg2d_phase_cycles(reset=True):
     """Cycles of the 2-D PCG phases (setup, sweeps, P1, P2); zeros unless built with -DVQPC_PHASE_TIMING."""
     out = (C.c_ulonglong * 4)()
     _check(load().vqpc_debug_pcg2d_phase_cycles(out, int(reset)))
+    return list(out)
+
+
+def pcg1d_phase_cycles(reset=True):
+    """Cycles between the 1-D PCG's barriers (Ap; update+residual+sweep 1; sweep 2; r.z); zeros unless
+    built with -DVQPC_PHASE_TIMING."""
+    out = (C.c_ulonglong * 4)()
+    _check(load().vqpc_debug_pcg1d_phase_cycles(out, int(reset)))
     return list(out)
 
 
