@@ -101,8 +101,9 @@ struct vqpc_ctx {
   // work buffers
   DBuf<double> xi, kappa, best, dvec;
   DBuf<uint8_t> kflag, status;
-  DBuf<int32_t> labels, perm, counts, iters, mia;
-  DBuf<int64_t> offsets, stats;
+  DBuf<int32_t> labels, perm, counts, iters, mia, keys, perm2;
+  DBuf<int64_t> offsets, stats, offsets2;
+  bool no_cost_order = getenv("VQPC_BUCKET_ORDER") != nullptr;  // diagnostics: label order only
   DBuf<double> rel, x;
   DBuf<int> counter, err;
   // optional per-kernel CUDA-event timing (bench roofline)
@@ -232,12 +233,9 @@ void run_realise(vqpc_ctx* c, const double* d_xi, int64_t B, int64_t ld, int K_u
   launch_check(c);
 }
 
-void run_bucket(vqpc_ctx* c, const int32_t* d_labels, int64_t B, int32_t* d_perm, int64_t* d_offsets) {
-  const int P = c->pb.P;
-  if (B <= 0) {
-    CK(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t) * (P + 2), c->stream));
-    return;
-  }
+// stable counting sort of ids (identity when d_ids is null) by keys[id] in [0, P) (P: invalid)
+void counting_sort(vqpc_ctx* c, const int32_t* d_keys, const int32_t* d_ids, int64_t B, int P, int32_t* d_perm,
+                   int64_t* d_offsets) {
   const int ntiles = static_cast<int>(ceil_div(B, BK_TILE));
   c->counts.ensure(static_cast<size_t>(P + 1) * ntiles);
   const size_t sm = sizeof(int32_t) * (P + 1);
@@ -245,14 +243,42 @@ void run_bucket(vqpc_ctx* c, const int32_t* d_labels, int64_t B, int32_t* d_perm
     CK(cudaFuncSetAttribute(bucket_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
     CK(cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
   }
-  Timed tm(c, VQPC_K_BUCKET);
-  bucket_hist_kernel<<<ntiles, 256, sm, c->stream>>>(d_labels, B, P, ntiles, c->counts.p);
+  bucket_hist_kernel<<<ntiles, 256, sm, c->stream>>>(d_keys, d_ids, B, P, ntiles, c->counts.p);
   launch_check(c);
   bucket_scan_kernel<<<1, 1024, 0, c->stream>>>(c->counts.p, static_cast<int64_t>(P + 1) * ntiles, P, ntiles,
                                                 d_offsets);
   launch_check(c);
-  bucket_scatter_kernel<<<ntiles, 32, sm, c->stream>>>(d_labels, B, P, ntiles, c->counts.p, d_perm);
+  bucket_scatter_kernel<<<ntiles, 32, sm, c->stream>>>(d_keys, d_ids, B, P, ntiles, c->counts.p, d_perm);
   launch_check(c);
+}
+
+void run_bucket(vqpc_ctx* c, const int32_t* d_labels, int64_t B, int32_t* d_perm, int64_t* d_offsets) {
+  const int P = c->pb.P;
+  if (B <= 0) {
+    CK(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t) * (P + 2), c->stream));
+    return;
+  }
+  Timed tm(c, VQPC_K_BUCKET);
+  counting_sort(c, d_labels, nullptr, B, P, d_perm, d_offsets);
+}
+
+// Solve order for the PCG work queue: label buckets (run_bucket), then a stable
+// pass by descending predicted cost (cost_key_kernel in bucket.cuh).
+void run_schedule(vqpc_ctx* c, const double* d_xi, int64_t ld, const int32_t* d_labels, int64_t B,
+                  const double* d_root) {
+  const int P = c->pb.P;
+  run_bucket(c, d_labels, B, c->perm.p, c->offsets.p);
+  if (B <= 0 || c->no_cost_order) return;
+  c->keys.ensure(B);
+  c->perm2.ensure(B);
+  c->offsets2.ensure(COST_BINS + 2);
+  Timed tm(c, VQPC_K_BUCKET);
+  cost_key_kernel<<<static_cast<unsigned>(ceil_div(B, 256)), 256, 0, c->stream>>>(
+      d_xi, ld, B, c->pb.n_kl, c->pb.m, d_labels, c->sqrt_lam.p, c->sites.p, d_root, c->keys.p);
+  launch_check(c);
+  counting_sort(c, c->keys.p, c->perm.p, B, COST_BINS, c->perm2.p, c->offsets2.p);
+  std::swap(c->perm, c->perm2);
+  (void)P;
 }
 
 void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d_kflag, const int32_t* d_perm,
@@ -469,7 +495,7 @@ void campaign_device(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, double 
     const int64_t nb = std::min(chunk, B - c0);
     const double* xi = d_xi + c0 * ld;
     run_assign(c, xi, nb, ld, root, c->sites.p, P, c->pb.m, d_labels + c0, nullptr);
-    run_bucket(c, d_labels + c0, nb, c->perm.p, c->offsets.p);
+    run_schedule(c, xi, ld, d_labels + c0, nb, root);
     CK(cudaMemsetAsync(c->kflag.p, 0, nb, c->stream));
     run_realise(c, xi, nb, ld, c->pb.n_kl, c->kappa.p, ldk, c->kflag.p);
     if (c0 >= solve_limit) {  // whole chunk beyond the solve subset: mark, skip the solver
@@ -596,8 +622,9 @@ void vqpc_ctx_destroy(vqpc_ctx* c) {
   c->fac.release();
   c->kflag.release();
   c->status.release();
-  for (auto* b : {&c->labels, &c->perm, &c->counts, &c->iters, &c->mia}) b->release();
+  for (auto* b : {&c->labels, &c->perm, &c->counts, &c->iters, &c->mia, &c->keys, &c->perm2}) b->release();
   c->offsets.release();
+  c->offsets2.release();
   c->stats.release();
   c->counter.release();
   c->err.release();
