@@ -216,6 +216,18 @@ def test_determinism_across_chunks():
         assert np.array_equal(a[k], b[k]), k
 
 
+@pytest.mark.parametrize("name,n_real", [("C2", 2048), ("C4s", 96)])
+def test_queue_order_does_not_change_results(name, n_real, monkeypatch):
+    """The longest-predicted-first work queue is pure scheduling: results equal a
+    label-ordered queue (VQPC_BUCKET_ORDER=1) bit for bit."""
+    cfg, basis, cb, xi = setup_case(name, n_real)
+    a = campaign.make_context(cfg, dict(basis=basis, codebook=cb)).run_campaign(xi, cfg["eps"])
+    monkeypatch.setenv("VQPC_BUCKET_ORDER", "1")
+    b = campaign.make_context(cfg, dict(basis=basis, codebook=cb)).run_campaign(xi, cfg["eps"])
+    for k in ("labels", "iterations", "rel", "status", "n_p", "sum_j", "conv_count", "conv_sum"):
+        assert np.array_equal(a[k], b[k]), k
+
+
 # ---------------------------------------------------------------- 2-D (C4) path
 def test_ic0_factor_and_apply_bit_identical():
     """Level-scheduled IC(0) on the GPU == the oracle's sequential IC(0), bit for bit,
