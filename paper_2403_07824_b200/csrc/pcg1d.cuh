@@ -9,9 +9,10 @@
 // dead and provably inert, see below). Registers per thread: x, r, p (R each),
 // the preconditioner couplings n_j and the transient w/z (or A p). Shared
 // memory is thread-major ([i*T + t] holds row tR+i, so warp accesses are
-// bank-conflict free): the sample's element conductances c_j = kappa_j/h, the
-// centroid factor {n_j, 1/u_j^2} and per-thread scan constants, reloaded only
-// when the bucket (label) changes.
+// bank-conflict free, 8 bytes per row and array): the sample's element
+// conductances c_j = kappa_j/h (the diagonal c_j + c_{j+1} is re-formed with the
+// same IEEE add wherever it is needed), the centroid factor's n_j and 1/u_j^2
+// and per-thread scan constants, reloaded only when the bucket (label) changes.
 //
 // Operator: A_jj = c_j + c_{j+1}, A_{j,j+1} = -c_{j+1}
 // with c_j = kappa_j / h — the same IEEE values the oracle's CSR holds; b_j = h.
@@ -54,11 +55,12 @@
 // same NWT = CL * NW warp values in the same order, so results are identical
 // to a single-CTA run of the same rows.
 //
-// Dead rows j >= n: n_j = 1/u_j^2 = 0 (so z_j = p_j = x_j = 0), n_{n-1} = 0,
-// d_j = 0 and the coupling c_j = 0 for j >= n (the diagonal of row n-1 keeps the
-// true c_n), so (A v)_j = 0 on dead rows without any masking; only b_j = 0 is
-// special, so the residual of the last warp (the only one that can own dead
-// rows) takes a masked code path behind a warp-uniform branch.
+// Dead rows j >= n: n_j = 1/u_j^2 = 0 (so z_j = p_j = x_j = 0) and n_{n-1} = 0.
+// Shared memory holds the conductances c_j for j <= n (c_n is the true right
+// conductance of row n-1, so d_{n-1} = c_{n-1} + c_n needs no special case;
+// its coupling term multiplies the dead p_n = 0) and 0 beyond. Only the last
+// warp can own dead rows, so A p and b - A x take a masked code path there
+// behind a warp-uniform branch (row n would otherwise see c_n).
 #pragma once
 #include <cooperative_groups.h>
 
@@ -113,10 +115,11 @@ template <int R, int T, int CL>
 struct Pcg1dShared {
   static constexpr int NW = T / 32;
   static constexpr int NWT = CL * NW;  // warps per sample (whole cluster)
-  double2 fac[R * T];     // {n_j, 1/u_j^2}, thread-major
-  double2 cd[R * T];      // {coupling c_j = kappa_j / h (0 for j >= n), diagonal d_j = c_j + c_{j+1}
-                          //  (true c_n; 0 for dead rows)}, thread-major
-  double cs_end;          // c_{R*T}: right coupling of the last thread's last row
+  double fn[R * T];       // factor couplings n_j, thread-major
+  double fu[R * T];       // factor pivots 1/u_j^2, thread-major
+  double c[R * T];        // element conductances c_j = kappa_j / h for j <= n (0 beyond), thread-major;
+                          // the diagonal d_j = c_j + c_{j+1} is formed on the fly (same IEEE add)
+  double cs_end;          // c_{R*T}: right conductance of the last thread's last row (0 beyond n)
   double lev[12 * T];     // per-thread lane-scan multipliers: L1[5], Q1, L2[5], Q2
   double qa[8 * T];       // per-thread quarter products: sweep 1 [0..3], sweep 2 [4..7]
   double2 f1[NWT], f2[NWT];   // per warp {product of the sweep multipliers (per centroid),
@@ -156,23 +159,51 @@ __device__ __forceinline__ double fused_row(double c_lo, double d, double c_hi, 
 // |b - A x|^2 over a thread's rows (4 split accumulators)
 template <int R, int T, bool MASK>
 __device__ __forceinline__ double true_residual(const double (&x)[R], double x_left, double x_right,
-                                                const double2* cdt, const double* c_halo, double h, int j0, int n) {
+                                                const double* ct, const double* c_halo, double h, int j0, int n) {
   constexpr int Q = R / 4;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  double2 cd_lo = cdt[0];
+  double c_lo = ct[0];
 #pragma unroll
   for (int i = 0; i < R; ++i) {
-    const double2 cd_hi = i + 1 < R ? cdt[(i + 1) * T] : make_double2(*c_halo, 0.0);
+    const double c_hi = i + 1 < R ? ct[(i + 1) * T] : *c_halo;
+    const double d = __dadd_rn(c_lo, c_hi);
     const double xl = i == 0 ? x_left : x[i - 1];
     const double xr = i + 1 < R ? x[i + 1] : x_right;
 #if VQPC_RESID_CSR
-    double rt = __dsub_rn(h, csr_row(cd_lo.x, cd_lo.y, cd_hi.x, xl, x[i], xr));
+    double rt = __dsub_rn(h, csr_row(c_lo, d, c_hi, xl, x[i], xr));
 #else
-    double rt = h - fused_row(cd_lo.x, cd_lo.y, cd_hi.x, xl, x[i], xr);
+    double rt = h - fused_row(c_lo, d, c_hi, xl, x[i], xr);
 #endif
     if (MASK && j0 + i >= n) rt = 0.0;
     acc[i / Q] = fma(rt, rt, acc[i / Q]);
-    cd_lo = cd_hi;
+    c_lo = c_hi;
+  }
+  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
+// A p over a thread's rows into wz, and the p.Ap partial (4 split accumulators).
+// Dead rows (j >= n, last warp only) are masked: row n's c_j is the true c_n.
+template <int R, int T, bool MASK>
+__device__ __forceinline__ double apply_rows(const double (&p)[R], double p_left, double p_right, const double* ct,
+                                             const double* c_halo, int j0, int n, double (&wz)[R]) {
+  constexpr int Q = R / 4;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  double c_lo = ct[0];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const double c_hi = i + 1 < R ? ct[(i + 1) * T] : *c_halo;
+    const double d = __dadd_rn(c_lo, c_hi);
+    const double pl = i == 0 ? p_left : p[i - 1];
+    const double pr = i + 1 < R ? p[i + 1] : p_right;
+#if VQPC_AP_CSR
+    double v = csr_row(c_lo, d, c_hi, pl, p[i], pr);
+#else
+    double v = fused_row(c_lo, d, c_hi, pl, p[i], pr);
+#endif
+    if (MASK && j0 + i >= n) v = 0.0;
+    wz[i] = v;
+    acc[i / Q] = fma(p[i], v, acc[i / Q]);
+    c_lo = c_hi;
   }
   return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
@@ -221,11 +252,11 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
                                                      (reinterpret_cast<char*>(local_arr) - reinterpret_cast<char*>(&S)))[idx] = v;
   };
   const int n = prm.n;
-  const double2* cdt = S.cd + tid;     // cdt[i*T] = {c_{j0+i}, d_{j0+i}}
+  const double* ct = S.c + tid;        // ct[i*T] = c_{j0+i}
   const double* levt = S.lev + tid;    // levt[k*T]
   const double* qat = S.qa + tid;      // qat[q*T]
-  const double2* fact = S.fac + tid;   // fact[i*T]
-  const double* c_halo = tid + 1 < T ? &S.cd[tid + 1].x : &S.cs_end;  // c_{j0+R}
+  const double* fut = S.fu + tid;      // fut[i*T] = 1/u_{j0+i}^2
+  const double* c_halo = tid + 1 < T ? &S.c[tid + 1] : &S.cs_end;  // c_{j0+R}
 
   if (prm.t_span && tid == 0) prm.t_span[2 * blockIdx.x] = globaltimer_ns();
   int cur_label = -1;
@@ -261,11 +292,15 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
     if (label != cur_label) {
       // ---- new bucket: factor to smem, per-thread / per-lane scan constants ----
       const double2* src = prm.factors + static_cast<size_t>(label) * prm.NP + static_cast<size_t>(rank) * R * T;
-      for (int e = tid; e < R * T; e += T) S.fac[(e % R) * T + e / R] = src[e];  // coalesced read
+      for (int e = tid; e < R * T; e += T) {  // coalesced read
+        const double2 f = src[e];
+        S.fn[(e % R) * T + e / R] = f.x;
+        S.fu[(e % R) * T + e / R] = f.y;
+      }
       __syncthreads();
 #pragma unroll
-      for (int i = 0; i < R; ++i) nc[i] = fact[i * T].x;
-      n_left = tid > 0 ? S.fac[(R - 1) * T + tid - 1].x : (j0 > 0 ? src[-1].x : 0.0);
+      for (int i = 0; i < R; ++i) nc[i] = S.fn[i * T + tid];
+      n_left = tid > 0 ? S.fn[(R - 1) * T + tid - 1] : (j0 > 0 ? src[-1].x : 0.0);
       double P1 = 1.0, P2 = 1.0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -303,16 +338,13 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
     const double* kap = prm.kappa + static_cast<size_t>(s) * prm.ldk;
     {
       // IEEE division: the oracle's kappa/h; d_j = c_j + c_{j+1} like its CSR diagonal
-      double c_prev = j0 < n ? kap[j0] / prm.h : 0.0;
 #pragma unroll
       for (int i = 0; i < R; ++i) {
         const int j = j0 + i;
-        const double c_next = j + 1 <= n ? kap[j + 1] / prm.h : 0.0;
-        S.cd[i * T + tid] = make_double2(j < n ? c_prev : 0.0, j < n ? __dadd_rn(c_prev, c_next) : 0.0);
-        c_prev = c_next;
+        S.c[i * T + tid] = j <= n ? kap[j] / prm.h : 0.0;
       }
-      // right coupling of this CTA's last row: c_{j0+R} (0 beyond the live rows)
-      if (tid == T - 1) S.cs_end = j0 + R < n ? kap[j0 + R] / prm.h : 0.0;
+      // right conductance of this CTA's last row: c_{j0+R} (0 beyond element n)
+      if (tid == T - 1) S.cs_end = j0 + R <= n ? kap[j0 + R] / prm.h : 0.0;
     }
     double x[R], r[R], p[R], wz[R];
     double bbq[4] = {0.0, 0.0, 0.0, 0.0};
@@ -375,7 +407,7 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) wz[q * Q + i] = fma(-nc[q * Q + i], wz[q * Q + i + 1], r[q * Q + i]);
 #pragma unroll
-        for (int i = 0; i < R; ++i) wz[i] *= fact[i * T].y;
+        for (int i = 0; i < R; ++i) wz[i] *= fut[i * T];
       }
       // the relative true residual decides convergence; its sqrt and division
       // overlap sweep 2, and the (warp-uniform) exit is taken after it
@@ -482,31 +514,10 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
         break;
       }
       {
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#if VQPC_AP_CSR
-        double2 cd_lo = cdt[0];
-#pragma unroll
-        for (int i = 0; i < R; ++i) {
-          const double2 cd_hi = i + 1 < R ? cdt[(i + 1) * T] : make_double2(*c_halo, 0.0);
-          const double pl = i == 0 ? p_left : p[i - 1];
-          const double pr = i + 1 < R ? p[i + 1] : p_right;
-          wz[i] = csr_row(cd_lo.x, cd_lo.y, cd_hi.x, pl, p[i], pr);
-          acc[i / Q] = fma(p[i], wz[i], acc[i / Q]);
-          cd_lo = cd_hi;
-        }
-#else
-        double2 cd_lo = cdt[0];
-#pragma unroll
-        for (int i = 0; i < R; ++i) {
-          const double2 cd_hi = i + 1 < R ? cdt[(i + 1) * T] : make_double2(*c_halo, 0.0);
-          const double pl = i == 0 ? p_left : p[i - 1];
-          const double pr = i + 1 < R ? p[i + 1] : p_right;
-          wz[i] = fused_row(cd_lo.x, cd_lo.y, cd_hi.x, pl, p[i], pr);  // (A p)_j, reusing wz
-          acc[i / Q] = fma(p[i], wz[i], acc[i / Q]);
-          cd_lo = cd_hi;
-        }
-#endif
-        const double a = warp_allsum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+        // dead rows (j >= n) only exist in the last warp: warp-uniform masked path
+        const double part = gwarp == NWT - 1 ? apply_rows<R, T, true>(p, p_left, p_right, ct, c_halo, j0, n, wz)
+                                             : apply_rows<R, T, false>(p, p_left, p_right, ct, c_halo, j0, n, wz);
+        const double a = warp_allsum(part);
         if (lane == 0) publish(S.red[0], gwarp, a);
         bar();  // barrier 1
         P1D_MARK(0);  // p update, A p, p.Ap
@@ -525,8 +536,8 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
       x_left = fma(alpha, p_left, x_left);
       x_right = fma(alpha, p_right, x_right);
       // true residual b - A x; dead rows (b_j = 0) only exist in the last warp
-      rr_loc = gwarp == NWT - 1 ? true_residual<R, T, true>(x, x_left, x_right, cdt, c_halo, prm.h, j0, n)
-                              : true_residual<R, T, false>(x, x_left, x_right, cdt, c_halo, prm.h, j0, n);
+      rr_loc = gwarp == NWT - 1 ? true_residual<R, T, true>(x, x_left, x_right, ct, c_halo, prm.h, j0, n)
+                              : true_residual<R, T, false>(x, x_left, x_right, ct, c_halo, prm.h, j0, n);
     }
 
     if (rank == 0 && tid == 0) {
