@@ -174,7 +174,9 @@ PcgVariant make_variant() {
 // smallest variant whose R*T*CL rows hold the n unknowns; n <= 4096 fits one SM's
 // register file (one CTA per sample), n <= 8192 uses a 2-CTA cluster
 const PcgVariant* pick_pcg(int n) {
-  static const PcgVariant table[] = {make_variant<16, 64, 1>(), make_variant<16, 128, 1>(),
+  // n <= 1024: 8 rows x 128 threads (4 warps beat 2 warps of 16 rows: C1 667k -> 735k samples/s);
+  // larger n: 16 rows per thread (C3 676k vs 475k, C2 190k vs 125k with 8 rows)
+  static const PcgVariant table[] = {make_variant<8, 128, 1>(), make_variant<16, 128, 1>(),
                                      make_variant<16, 256, 1>(), make_variant<16, 256, 2>()};
   // experiments: VQPC_PCG_R=8 selects the 8-rows-per-thread layout (twice the warps)
   static const PcgVariant table8[] = {make_variant<8, 128, 1>(), make_variant<8, 256, 1>(),
