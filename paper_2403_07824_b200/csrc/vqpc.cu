@@ -488,25 +488,55 @@ void campaign_device(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, double 
   const int P = c->pb.P;
   if (chunk <= 0 || chunk > B) chunk = B;
   const int64_t ldk = kappa_ld(c);
-  c->kappa.ensure(static_cast<size_t>(std::max<int64_t>(chunk, 1)) * ldk);
-  c->kflag.ensure(std::max<int64_t>(chunk, 1));
-  c->perm.ensure(std::max<int64_t>(chunk, 1));
-  c->offsets.ensure(P + 2);
   const double* root = c->pb.method == VQPC_GRID || c->pb.method == VQPC_SIGN_GRID ? nullptr : c->root.p;
+  // Samples [0, nsolve) are solved. When that range spans several chunks, their
+  // kappa rows are kept and solved by ONE PCG launch after the chunk loop (one
+  // work-queue tail instead of one per chunk; C5: 4 launches -> 1) as long as the
+  // rows fit a fixed budget; otherwise every chunk is solved as it is realised.
+  const int64_t nsolve = std::min<int64_t>(B, std::max<int64_t>(solve_limit, 0));
+  constexpr double kMergeBudget = 16e9;  // bytes of kept kappa rows
+  const bool merge = chunk < B && nsolve > chunk &&
+                     static_cast<double>(nsolve) * static_cast<double>(ldk) * 8.0 <= kMergeBudget;
+  const int64_t keep = merge ? nsolve : 0;  // kept rows (merged solve)
+  c->kappa.ensure(static_cast<size_t>(std::max<int64_t>(keep + chunk, 1)) * ldk);
+  c->kflag.ensure(std::max<int64_t>(keep + chunk, 1));
+  c->perm.ensure(std::max<int64_t>(std::max(keep, chunk), 1));
+  c->offsets.ensure(P + 2);
+  double* const kappa_scratch = c->kappa.p + static_cast<size_t>(keep) * ldk;  // rows of unsolved chunks
+  uint8_t* const kflag_scratch = c->kflag.p + keep;
+  if (merge) CK(cudaMemsetAsync(c->kflag.p, 0, keep, c->stream));
   for (int64_t c0 = 0; c0 < B; c0 += chunk) {
     const int64_t nb = std::min(chunk, B - c0);
     const double* xi = d_xi + c0 * ld;
     run_assign(c, xi, nb, ld, root, c->sites.p, P, c->pb.m, d_labels + c0, nullptr);
-    run_schedule(c, xi, ld, d_labels + c0, nb, root);
-    CK(cudaMemsetAsync(c->kflag.p, 0, nb, c->stream));
-    run_realise(c, xi, nb, ld, c->pb.n_kl, c->kappa.p, ldk, c->kflag.p);
+    const bool kept = merge && c0 < nsolve;  // rows [c0, c0 + nb) land in the kept buffer
+    double* kap = kept ? c->kappa.p + static_cast<size_t>(c0) * ldk : kappa_scratch;
+    uint8_t* kfl = kept ? c->kflag.p + c0 : kflag_scratch;
+    if (!kept) CK(cudaMemsetAsync(kfl, 0, nb, c->stream));
+    run_realise(c, xi, nb, ld, c->pb.n_kl, kap, ldk, kfl);
+    if (merge) {
+      // beyond the solve subset: mark here; solved rows wait for the merged launch
+      const int64_t u0 = std::max(c0, nsolve), u1 = c0 + nb;
+      if (u1 > u0) {
+        mark_unsolved_kernel<<<static_cast<unsigned>(ceil_div(u1 - u0, 256)), 256, 0, c->stream>>>(
+            d_iters + u0, d_rel + u0, d_status + u0, u1 - u0);
+        launch_check(c);
+      }
+      continue;
+    }
     if (c0 >= solve_limit) {  // whole chunk beyond the solve subset: mark, skip the solver
       mark_unsolved_kernel<<<static_cast<unsigned>(ceil_div(nb, 256)), 256, 0, c->stream>>>(
           d_iters + c0, d_rel + c0, d_status + c0, nb);
       launch_check(c);
       continue;
     }
-    run_pcg(c, c->kappa.p, ldk, c->kflag.p, c->perm.p, d_labels + c0, nb, c0, eps, max_iter, nullptr, d_iters,
+    run_schedule(c, xi, ld, d_labels + c0, nb, root);
+    run_pcg(c, kap, ldk, kfl, c->perm.p, d_labels + c0, nb, c0, eps, max_iter, nullptr, d_iters, d_rel, d_status,
+            nullptr, solve_limit);
+  }
+  if (merge) {
+    run_schedule(c, d_xi, ld, d_labels, nsolve, root);
+    run_pcg(c, c->kappa.p, ldk, c->kflag.p, c->perm.p, d_labels, nsolve, 0, eps, max_iter, nullptr, d_iters,
             d_rel, d_status, nullptr, solve_limit);
   }
   CK(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 4 * P, c->stream));
