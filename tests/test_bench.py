@@ -1,0 +1,93 @@
+"""bench.py host logic (no GPU): workload description per config, roofline
+arithmetic for every dominant-kernel kind, CPU sample sizing, and the JSON
+contract of the reference arm's line."""
+import importlib.util
+import json
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _bench():
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_workload_describes_config(name):
+    from paper_2403_07824_b200 import campaign
+    b = _bench()
+    cfg = campaign.CONFIGS[name]
+    w = b.workload(cfg, cfg["n_realizations"], cfg["n_kl"])
+    n = (cfg["mesh_resolution"] - 1) ** cfg["dim"]
+    assert w["unknowns"] == n and w["P"] == cfg["quantizer"]["P"] and w["d"] == cfg["m"]
+    assert w["workload"].startswith(name + ":")
+    assert ("IC(0)" in w["workload"]) == (cfg["dim"] == 2)
+    assert (w["solve_subset"] is not None) == (name == "C5")
+    json.dumps(w)
+
+
+def test_cpu_sample_size_bounded():
+    from paper_2403_07824_b200 import campaign
+    b = _bench()
+    sizes = {k: b.cpu_sample_size(campaign.CONFIGS[k]) for k in ("C1", "C2", "C3", "C4", "C5")}
+    assert sizes["C4"] <= 64 and sizes["C2"] <= 1024 and all(v >= 16 for v in sizes.values())
+
+
+def _prof(kind, ms, launches=3):
+    p = {k: {"ms": 0.0, "launches": 0} for k in ("assign", "bucket", "realise", "pcg", "other")}
+    p[kind] = {"ms": ms, "launches": launches}
+    return p
+
+
+def test_roofline_pcg2d_is_hbm_bound(monkeypatch):
+    from paper_2403_07824_b200 import campaign
+    b = _bench()
+    monkeypatch.setattr(b, "measured_peaks", lambda: {"hbm_gbs": 6536.4})
+    cfg = campaign.CONFIGS["C4"]
+    r = cfg["mesh_resolution"]
+    n, npts = (r - 1) ** 2, (r + 1) ** 2
+    iters = 1000
+    roof = b.roofline(cfg, _prof("pcg", 3 * 1000.0), iters, 8, 3, 0)  # 1 s per launch
+    assert roof["kernel"] == "pcg2d" and roof["bound"] == "hbm" and roof["unit"] == "GB/s"
+    assert roof["achieved"] == pytest.approx(8.0 * (2 * npts + 14 * n) * iters / 1e9)
+    assert roof["frac"] == pytest.approx(roof["achieved"] / 6536.4)
+
+
+def test_roofline_pcg1d_and_realise_fp64(monkeypatch):
+    from paper_2403_07824_b200 import campaign, lib
+    b = _bench()
+    monkeypatch.setattr(lib, "fp64_peak", lambda device=0: 33.5)
+    cfg = campaign.CONFIGS["C2"]
+    n = cfg["mesh_resolution"] - 1
+    roof = b.roofline(cfg, _prof("pcg", 3 * 500.0), 10 ** 6, 1 << 17, 3, 0)
+    assert roof["kernel"] == "pcg1d" and roof["bound"] == "fp64"
+    assert roof["achieved"] == pytest.approx(31.0 * n * 1e6 / 0.5 / 1e12)
+    assert roof["frac"] == pytest.approx(roof["achieved"] / 33.5)
+    cfg5 = campaign.CONFIGS["C5"]
+    roof = b.roofline(cfg5, _prof("realise", 3 * 100.0), 0, 1 << 14, 3, 0)
+    assert roof["kernel"] == "realise"
+    assert roof["achieved"] == pytest.approx(2.0 * cfg5["mesh_resolution"] * cfg5["n_kl"] * (1 << 14) / 0.1 / 1e12)
+
+
+def test_reference_arm_contract(monkeypatch, capsys):
+    """--impl reference on rank != 0 exits without output; rank 0 prints the
+    contract keys (timed on a tiny C1 sample through the oracle)."""
+    b = _bench()
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--impl", "reference", "--config", "C1", "--steps", "1",
+                                      "--warmup", "0", "--cpu-samples", "16"])
+    args = b.parse()
+    b.run_reference(args, rank=1, world=2)
+    assert capsys.readouterr().out == ""
+    b.run_reference(args, rank=0, world=1)
+    line = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "impl", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["e2e"]["h2d_bytes_per_step"] == 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["value"] > 0
