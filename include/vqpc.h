@@ -105,9 +105,13 @@ const char* vqpc_error_string(int code);
 /* Run all work of this context on an existing cudaStream_t (NULL: own stream). */
 int vqpc_set_stream(vqpc_ctx* ctx, void* cuda_stream);
 int vqpc_synchronize(vqpc_ctx* ctx);
-/* 2-D solver: enable != 0 sums every dot product serially in natural order
- * (solver.cpp:176-180), making the whole solve bit-identical to the reference
- * arithmetic at some cost; default 0 = block-tree reductions. No effect in 1-D. */
+/* Reference-order mode (parity instrument). enable != 0: every dot product is
+ * summed serially in natural order (solver.cpp:176-180); in 1-D the solve also
+ * runs Eigen's LL^T triangular solves on the reversed order (solver.cpp:98-110)
+ * and the unfused vector updates (solver.cpp:224-241) on one thread per sample
+ * (pcg1d_exact_kernel, ~0.5 ms per iteration at n = 4095). Either way the solve
+ * is bit-identical to the reference arithmetic given the same coefficient bits.
+ * Default 0 = the throughput kernels (block-tree reductions, chunked scans). */
 int vqpc_set_exact_reductions(vqpc_ctx* ctx, int enable);
 /* unknowns per sample system (n) and the number of device kernel launches
  * issued by this context so far (bench evidence). */

@@ -12,14 +12,16 @@
 // u and l are bit-identical to the oracle's factor of the same kappa. The
 // stored form is the unit-bidiagonal split U = (I+N) D used by pcg1d:
 //   n_j = l_j / u_{j+1}  (n_{n-1} = 0),   dinv2_j = 1 / u_j^2;  dead rows {0,0}.
-// One thread per centroid (one-time setup; latency-bound by design).
+// One thread per centroid (one-time setup; latency-bound by design). With lu_out
+// the pass-1 values {l_j, u_j} are kept as well (pcg1d_exact_kernel applies them
+// exactly as the reference's SimplicialLLT solve does).
 #pragma once
 #include "common.cuh"
 
 namespace vqpc {
 
 static __global__ void factor1d_kernel(const double* kappa, int64_t ldk, int P, int n, double h, double2* fac, int NP,
-                                int* err) {
+                                int* err, double2* lu_out = nullptr) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
   const double* kp = kappa + static_cast<size_t>(p) * ldk;
@@ -41,6 +43,7 @@ static __global__ void factor1d_kernel(const double* kappa, int64_t ldk, int P, 
     if (!(d > 0.0)) ok = false;
     const double u = __dsqrt_rn(d);
     f[j] = make_double2(l, u);
+    if (lu_out) lu_out[static_cast<size_t>(p) * NP + j] = make_double2(l, u);  // reference-order mode
     u_next = u;
     s_next = s_j;
   }

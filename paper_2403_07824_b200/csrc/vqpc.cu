@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "factor.cuh"
 #include "pcg1d.cuh"
+#include "pcg1d_exact.cuh"
 #include "pcg2d.cuh"
 #include "realise.cuh"
 #include "vqpc.h"
@@ -97,7 +98,10 @@ struct vqpc_ctx {
   Grid2D g2{};
   DBuf<double> fac2, work2;
   DBuf<int> gmap;
-  int exact = 0;  // 2-D: serial (reference-order) dot products
+  int exact = 0;  // reference-order mode: serial dot products (2-D); 1-D: pcg1d_exact_kernel
+  DBuf<double2> fac_lu;  // 1-D reference-order mode: P x NP {l_j, u_j}, built on first use
+  bool have_lu = false;
+  DBuf<double> work1x;
   // work buffers
   DBuf<double> xi, kappa, best, dvec;
   DBuf<uint8_t> kflag, status;
@@ -181,8 +185,13 @@ const PcgVariant* pick_pcg(int n) {
   // experiments: VQPC_PCG_R=8 selects the 8-rows-per-thread layout (twice the warps)
   static const PcgVariant table8[] = {make_variant<8, 128, 1>(), make_variant<8, 256, 1>(),
                                       make_variant<8, 512, 1>(), make_variant<8, 512, 2>()};
+  // experiments: VQPC_PCG_SPLIT=1 spreads n in (2048, 4096] over a 2-CTA cluster of 128-thread
+  // CTAs (two half-samples per SM; same warp layout, so results are bit-identical)
+  static const PcgVariant split2 = make_variant<16, 128, 2>();
   const char* env = std::getenv("VQPC_PCG_R");
   const bool r8 = env && std::atoi(env) == 8;
+  const char* sp = std::getenv("VQPC_PCG_SPLIT");
+  if (sp && std::atoi(sp) == 1 && n > 2048 && n <= 4096) return &split2;
   for (const auto& v : (r8 ? table8 : table))
     if (n <= v.R * v.T * v.CL) return &v;
   return nullptr;
@@ -328,6 +337,58 @@ void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d
   launch_check(c);
 }
 
+// 1-D reference-order mode (vqpc_set_exact_reductions): the serial-arithmetic
+// instrument kernel; the factor's pass-1 values {l_j, u_j} are produced by the
+// same factor1d_kernel on first use.
+void run_pcg1d_exact(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d_kflag, const int32_t* d_perm,
+                     const int32_t* d_labels, int64_t B, int64_t out_base, double eps, int max_iter,
+                     const int32_t* d_mia, int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x,
+                     int64_t solve_limit) {
+  const int P = c->pb.P, n = c->n;
+  if (!c->have_lu) {
+    c->fac_lu.ensure(static_cast<size_t>(P) * c->NP);
+    CK(cudaMemsetAsync(c->err.p, 0, sizeof(int), c->stream));
+    Timed tm(c, VQPC_K_OTHER);
+    factor1d_kernel<<<static_cast<unsigned>(ceil_div(P, 64)), 64, 0, c->stream>>>(
+        c->kappa_c.p, (c->pb.n_nodes + 1) & ~1, P, n, h_of(c->pb), c->fac.p, c->NP, c->err.p, c->fac_lu.p);
+    launch_check(c);
+    c->have_lu = true;
+  }
+  int per_sm = 0;
+  const size_t smem = sizeof(double) * n;
+  CK(cudaFuncSetAttribute(pcg1d_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg1d_exact_kernel, PX_T, smem));
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(B, static_cast<int64_t>(per_sm) * c->sm_count));
+  c->work1x.ensure(static_cast<size_t>(blocks) * (6 * static_cast<size_t>(n) + 1));
+  c->counter.ensure(1);
+  CK(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->stream));
+  Pcg1dExactParams prm{};
+  prm.n = n;
+  prm.h = h_of(c->pb);
+  prm.kappa = d_kappa;
+  prm.ldk = ldk;
+  prm.kflag = d_kflag;
+  prm.perm = d_perm;
+  prm.labels = d_labels;
+  prm.lu = c->fac_lu.p;
+  prm.NP = c->NP;
+  prm.B = B;
+  prm.out_base = out_base;
+  prm.solve_limit = solve_limit;
+  prm.eps = eps;
+  prm.max_iter = max_iter;
+  prm.max_iter_arr = d_mia;
+  prm.counter = c->counter.p;
+  prm.iters = d_iters;
+  prm.rel = d_rel;
+  prm.status = d_status;
+  prm.x_out = d_x;
+  prm.work = c->work1x.p;
+  Timed tm(c, VQPC_K_PCG);
+  pcg1d_exact_kernel<<<static_cast<unsigned>(blocks), PX_T, smem, c->stream>>>(prm);
+  launch_check(c);
+}
+
 void run_pcg(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d_kflag, const int32_t* d_perm,
              const int32_t* d_labels, int64_t B, int64_t out_base, double eps, int max_iter, const int32_t* d_mia,
              int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x,
@@ -336,6 +397,11 @@ void run_pcg(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d_k
   if (c->pb.dim == 2) {
     run_pcg2d(c, d_kappa, ldk, d_kflag, d_perm, d_labels, B, out_base, eps, max_iter, d_mia, d_iters, d_rel,
               d_status, d_x, solve_limit);
+    return;
+  }
+  if (c->exact) {
+    run_pcg1d_exact(c, d_kappa, ldk, d_kflag, d_perm, d_labels, B, out_base, eps, max_iter, d_mia, d_iters, d_rel,
+                    d_status, d_x, solve_limit);
     return;
   }
   const PcgVariant* v = pick_pcg(c->n);
@@ -652,6 +718,8 @@ void vqpc_ctx_destroy(vqpc_ctx* c) {
                   &c->rel, &c->x, &c->fac2, &c->work2})
     b->release();
   c->fac.release();
+  c->fac_lu.release();
+  c->work1x.release();
   c->kflag.release();
   c->status.release();
   for (auto* b : {&c->labels, &c->perm, &c->counts, &c->iters, &c->mia, &c->keys, &c->perm2}) b->release();
@@ -742,6 +810,7 @@ int vqpc_factor_centroids(vqpc_ctx* c) {
       if (f) throw ApiError{VQPC_COEFFICIENT_OVERFLOW, "coefficient-overflow in a centroid coefficient"};
     if (err) throw ApiError{VQPC_NOT_SPD, "not-spd"};
     c->factored = true;
+    c->have_lu = false;  // reference-order 1-D factor values are rebuilt on first use
   });
 }
 

@@ -287,3 +287,29 @@ def test_2d_fast_mode_statistics():
     assert cmp["status_agree"] >= 0.99
     assert abs(cmp["mean_cpu"] - cmp["mean_gpu"]) / cmp["mean_cpu"] < 0.01
     assert cmp["max_dj"] <= 6
+
+
+@pytest.mark.parametrize("name,n_real", [("C1", 128), ("C2", 48), ("C3", 64), ("C5", 16)])
+def test_1d_exact_mode_bit_identical(name, n_real):
+    """1-D reference-order mode (pcg1d_exact_kernel): serial natural-order dots,
+    Eigen's LL^T solves on the reversed order, unfused vector updates. Given the
+    same coefficient bits, J, status, the final residual record and x are
+    bit-identical to the CPU oracle — so the fast kernel's differences come only
+    from its reduction/scan order and its FMA updates."""
+    cfg, basis, cb, xi = setup_case(name, n_real)
+    ocb = oracle_codebook(cb)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    ctx.set_exact_reductions(True)
+    kc = ctx.centroid_coefficients()
+    labels = oracle.assign(ocb, xi)
+    kap_gpu, _ = ctx.realise(xi)
+    pset = oracle.PreconditionerSet.from_coefficients(1, cfg["mesh_resolution"], "cholesky", kc)
+    cap = 1200  # bounds the serial instrument's run time on stagnating samples
+    it, rel, st, x = ctx.solve_batch(xi, labels, cfg["eps"], max_iter=cap, want_x=True)
+    for i in range(len(xi)):
+        out = pset.pcg(int(labels[i]), kap_gpu[i, :cfg["mesh_resolution"]], cfg["eps"], max_iter=cap)
+        assert out["iterations"] == it[i] and out["status"] == st[i], (i, out["iterations"], it[i])
+        assert out["rel"] == rel[i], i
+        assert np.array_equal(out["x"], x[i]), i
+    print(name, "exact mode: %d samples bit-identical, J mean %.2f, statuses %s" % (
+        len(xi), it.mean(), np.bincount(st)))
