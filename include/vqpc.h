@@ -134,7 +134,10 @@ int vqpc_assign_d(vqpc_ctx* ctx, const double* d_xi, int64_t B, int ld, int32_t*
  * has P+1 entries (group p = perm[offsets[p] .. offsets[p+1])). ----------- */
 int vqpc_bucket_d(vqpc_ctx* ctx, const int32_t* d_labels, int64_t B, int32_t* d_perm, int64_t* d_offsets);
 
-/* ---- (a) realisation: kappa_i = transport(lift(basis, xi_i[0:m])) -------- */
+/* ---- (a) realisation: kappa_i = transport(lift(basis, xi_i[0:m])) --------
+ * status_out[i] (nullable): 0, VQPC_S_COEFF_OVERFLOW (a non-finite kappa:
+ * transport's coefficient-overflow, field.cpp:141-142) or VQPC_S_INVALID_COEFF
+ * (kappa == 0 after exp underflow: assembly's invalid-coefficient). */
 int vqpc_realise(vqpc_ctx* ctx, const double* xi, int64_t B, int ld, int m, double* kappa_out,
                  uint8_t* status_out);
 

@@ -40,8 +40,9 @@ class OracleError(RuntimeError):
 
 def build(force: bool = False) -> None:
     """Compile liboracle.so (and oracle/_ref when /root/reference exists)."""
-    if force or not os.path.exists(LIB_PATH) or not os.path.exists(FMA_PATH):
-        subprocess.check_call(["make", "-s", "-C", HERE, "liboracle.so", "liboracle_fma.so"])
+    # make tracks the sources' timestamps (a stale build would check the GPU
+    # against an outdated restatement)
+    subprocess.check_call(["make", "-s", "-C", HERE, "liboracle.so", "liboracle_fma.so"] + (["-B"] if force else []))
     if os.path.isdir("/root/reference/proj") and (force or not os.path.exists(REF_PATH)):
         subprocess.check_call(["make", "-s", "-C", os.path.join(HERE, "ref")])
 

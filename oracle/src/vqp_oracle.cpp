@@ -776,8 +776,9 @@ static void solve_one(const Model& model, const Basis& basis, const double* xi, 
                       const Preconditioner& M, double eps, int max_iter, Record& rec, double* x_out,
                       std::vector<double>& h) {
   try {
-    for (int k = 0; k < m_xi; ++k)
-      if (!std::isfinite(xi[k])) throw Err(INVALID_LATENT);
+    // no finiteness check here: like the reference (driver.cpp:230-233), a
+    // non-finite xi_k reaches lift and transport reports coefficient-overflow
+    // (only assign's first m components raise invalid-latent)
     lift(basis.evals, basis.evecs, basis.n_nodes, xi, m_xi, h.data());
     transport(h.data(), basis.n_nodes);
     const System sys = model.assemble(h.data());

@@ -261,8 +261,8 @@ __device__ __forceinline__ double tree_sum(const double* part) {
   return v[0];
 }
 
-template <int R, int T, int CL>
-__global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
+template <int R, int T, int CL, int MINB = 1>
+__global__ void __launch_bounds__(T, MINB) pcg1d_kernel(const Pcg1dParams prm) {
   using Sh = Pcg1dShared<R, T, CL>;
   constexpr int NW = Sh::NW;
   constexpr int NWT = Sh::NWT;
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(T, 1) pcg1d_kernel(const Pcg1dParams prm) {
         prm.rel[gs] = 0.0;
         prm.status[gs] = gs >= prm.solve_limit ? VQPC_S_NOT_SOLVED
                          : label < 0           ? VQPC_S_INVALID_LATENT
-                                               : VQPC_S_COEFF_OVERFLOW;
+                                               : (prm.kflag[s] & 1) ? VQPC_S_COEFF_OVERFLOW : VQPC_S_INVALID_COEFF;
       }
       continue;
     }

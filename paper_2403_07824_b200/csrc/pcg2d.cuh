@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
         prm.rel[gs] = 0.0;
         prm.status[gs] = gs >= prm.solve_limit ? VQPC_S_NOT_SOLVED
                          : label < 0           ? VQPC_S_INVALID_LATENT
-                                               : VQPC_S_COEFF_OVERFLOW;
+                                               : (prm.kflag[s] & 1) ? VQPC_S_COEFF_OVERFLOW : VQPC_S_INVALID_COEFF;
       }
       continue;
     }

@@ -38,7 +38,8 @@ struct RealiseParams {
   int K_use;               // modes lifted (m)
   double* kappa;           // B x ldk
   int64_t ldk;
-  uint8_t* flag;           // per sample; set to 1 on a non-finite kappa (nullable)
+  uint8_t* flag;           // per sample, ORed: 1 non-finite kappa (transport's coefficient-overflow),
+                           // 2 kappa == 0 (assembly's invalid-coefficient); nullable
 };
 
 static __global__ void __launch_bounds__(RL_THREADS) realise_kernel(const RealiseParams prm) {
@@ -95,7 +96,7 @@ static __global__ void __launch_bounds__(RL_THREADS) realise_kernel(const Realis
   for (int a = 0; a < 4; ++a) {
     const int64_t b = b0 + wm * 32 + a * 8 + (lane >> 2);
     if (b >= prm.B) continue;
-    bool bad = false;
+    unsigned bad = 0;  // bit 0: non-finite kappa (transport), bit 1: kappa == 0 (assembly)
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int i = i0 + wn * 32 + c * 8 + 2 * (lane & 3);
@@ -103,7 +104,7 @@ static __global__ void __launch_bounds__(RL_THREADS) realise_kernel(const Realis
       const double k1v = exp(acc[a][c][1]);
       double* dst = prm.kappa + b * prm.ldk + i;
       if (i + 1 < prm.n_nodes) {
-        bad |= !isfinite(k0v) || !isfinite(k1v);
+        bad |= (!isfinite(k0v) || !isfinite(k1v) ? 1u : 0u) | (k0v == 0.0 || k1v == 0.0 ? 2u : 0u);
         if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
           *reinterpret_cast<double2*>(dst) = make_double2(k0v, k1v);
         } else {
@@ -111,11 +112,15 @@ static __global__ void __launch_bounds__(RL_THREADS) realise_kernel(const Realis
           dst[1] = k1v;
         }
       } else if (i < prm.n_nodes) {
-        bad |= !isfinite(k0v);
+        bad |= (!isfinite(k0v) ? 1u : 0u) | (k0v == 0.0 ? 2u : 0u);
         dst[0] = k0v;
       }
     }
-    if (bad && prm.flag) prm.flag[b] = 1;
+    if (bad && prm.flag) {  // several lanes / CTAs flag one sample: OR into the byte atomically
+      uint8_t* fp = prm.flag + b;
+      const uintptr_t a = reinterpret_cast<uintptr_t>(fp);
+      atomicOr(reinterpret_cast<unsigned*>(a & ~static_cast<uintptr_t>(3)), bad << (8 * (a & 3)));
+    }
   }
 }
 

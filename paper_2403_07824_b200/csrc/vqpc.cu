@@ -170,9 +170,9 @@ struct PcgVariant {
   size_t smem;
 };
 
-template <int R, int T, int CL>
+template <int R, int T, int CL, int MINB = 1>
 PcgVariant make_variant() {
-  return PcgVariant{R, T, CL, &pcg1d_kernel<R, T, CL>, pcg1d_smem_bytes<R, T, CL>()};
+  return PcgVariant{R, T, CL, &pcg1d_kernel<R, T, CL, MINB>, pcg1d_smem_bytes<R, T, CL>()};
 }
 
 // smallest variant whose R*T*CL rows hold the n unknowns; n <= 4096 fits one SM's
@@ -188,6 +188,10 @@ const PcgVariant* pick_pcg(int n) {
   // experiments: VQPC_PCG_SPLIT=1 spreads n in (2048, 4096] over a 2-CTA cluster of 128-thread
   // CTAs (two half-samples per SM; same warp layout, so results are bit-identical)
   static const PcgVariant split2 = make_variant<16, 128, 2>();
+  // experiments: VQPC_PCG_OCC4=1 caps n <= 1024 at 128 registers (4 CTAs = 16 warps per SM)
+  static const PcgVariant occ4 = make_variant<8, 128, 1, 4>();
+  const char* o4 = std::getenv("VQPC_PCG_OCC4");
+  if (o4 && std::atoi(o4) == 1 && n <= 1024) return &occ4;
   const char* env = std::getenv("VQPC_PCG_R");
   const bool r8 = env && std::atoi(env) == 8;
   const char* sp = std::getenv("VQPC_PCG_SPLIT");
@@ -565,7 +569,7 @@ void campaign_device(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, double 
                      static_cast<double>(nsolve) * static_cast<double>(ldk) * 8.0 <= kMergeBudget;
   const int64_t keep = merge ? nsolve : 0;  // kept rows (merged solve)
   c->kappa.ensure(static_cast<size_t>(std::max<int64_t>(keep + chunk, 1)) * ldk);
-  c->kflag.ensure(std::max<int64_t>(keep + chunk, 1));
+  c->kflag.ensure(static_cast<size_t>(std::max<int64_t>(keep + chunk, 1)) + 4);  // + 4: word-wide atomicOr flags
   c->perm.ensure(std::max<int64_t>(std::max(keep, chunk), 1));
   c->offsets.ensure(P + 2);
   double* const kappa_scratch = c->kappa.p + static_cast<size_t>(keep) * ldk;  // rows of unsolved chunks
@@ -607,6 +611,7 @@ void campaign_device(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, double 
   }
   CK(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 4 * P, c->stream));
   CK(cudaMemsetAsync(d_summary, 0, sizeof(int64_t) * 4, c->stream));
+  if (B <= 0) return;  // empty batch: zero statistics
   Timed tm(c, VQPC_K_OTHER);
   stats_kernel<<<static_cast<unsigned>(ceil_div(B, 256)), 256, 0, c->stream>>>(
       d_labels, d_iters, d_status, B, P, reinterpret_cast<unsigned long long*>(d_stats),
@@ -783,7 +788,7 @@ int vqpc_factor_centroids(vqpc_ctx* c) {
     h2d(c, c->xi.p, chi.data(), chi.size());
     const int64_t ldk = kappa_ld(c);
     c->kappa_c.ensure(static_cast<size_t>(P) * ldk);
-    c->kflag.ensure(P);
+    c->kflag.ensure(static_cast<size_t>(P) + 4);  // + 4: word-wide atomicOr flags
     CK(cudaMemsetAsync(c->kflag.p, 0, P, c->stream));
     run_realise(c, c->xi.p, P, std::max(m, 1), m, c->kappa_c.p, ldk, c->kflag.p);
     c->err.ensure(1);
@@ -806,8 +811,10 @@ int vqpc_factor_centroids(vqpc_ctx* c) {
     d2h(c, &err, c->err.p, 1);
     d2h(c, flags.data(), c->kflag.p, P);
     CK(cudaStreamSynchronize(c->stream));
-    for (uint8_t f : flags)
-      if (f) throw ApiError{VQPC_COEFFICIENT_OVERFLOW, "coefficient-overflow in a centroid coefficient"};
+    for (uint8_t f : flags) {
+      if (f & 1) throw ApiError{VQPC_COEFFICIENT_OVERFLOW, "coefficient-overflow in a centroid coefficient"};
+      if (f) throw ApiError{VQPC_INVALID_COEFFICIENT, "invalid-coefficient (kappa underflow) in a centroid coefficient"};
+    }
     if (err) throw ApiError{VQPC_NOT_SPD, "not-spd"};
     c->factored = true;
     c->have_lu = false;  // reference-order 1-D factor values are rebuilt on first use
@@ -879,7 +886,7 @@ int vqpc_realise(vqpc_ctx* c, const double* xi, int64_t B, int ld, int m, double
     const int64_t ldk = kappa_ld(c);
     c->xi.ensure(static_cast<size_t>(std::max<int64_t>(B, 1)) * ld);
     c->kappa.ensure(static_cast<size_t>(std::max<int64_t>(B, 1)) * ldk);
-    c->kflag.ensure(std::max<int64_t>(B, 1));
+    c->kflag.ensure(static_cast<size_t>(std::max<int64_t>(B, 1)) + 4);  // + 4: word-wide atomicOr flags
     h2d(c, c->xi.p, xi, static_cast<size_t>(B) * ld);
     CK(cudaMemsetAsync(c->kflag.p, 0, std::max<int64_t>(B, 1), c->stream));
     run_realise(c, c->xi.p, B, ld, m, c->kappa.p, ldk, c->kflag.p);
@@ -888,7 +895,8 @@ int vqpc_realise(vqpc_ctx* c, const double* xi, int64_t B, int ld, int m, double
     if (status_out) {
       d2h(c, status_out, c->kflag.p, B);
       CK(cudaStreamSynchronize(c->stream));
-      for (int64_t i = 0; i < B; ++i) status_out[i] = status_out[i] ? VQPC_S_COEFF_OVERFLOW : 0;
+      for (int64_t i = 0; i < B; ++i)
+        status_out[i] = (status_out[i] & 1) ? VQPC_S_COEFF_OVERFLOW : status_out[i] ? VQPC_S_INVALID_COEFF : 0;
     }
     CK(cudaStreamSynchronize(c->stream));
   });
@@ -912,7 +920,7 @@ int vqpc_solve_batch(vqpc_ctx* c, const double* xi, int64_t B, int ld, const int
     c->perm.ensure(Bm);
     c->offsets.ensure(P + 2);
     c->kappa.ensure(static_cast<size_t>(Bm) * ldk);
-    c->kflag.ensure(Bm);
+    c->kflag.ensure(static_cast<size_t>(Bm) + 4);  // + 4: word-wide atomicOr flags
     c->iters.ensure(Bm);
     c->rel.ensure(Bm);
     c->status.ensure(Bm);

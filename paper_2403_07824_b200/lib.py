@@ -220,7 +220,8 @@ class Context:
         self._c(load().vqpc_synchronize(self.h))
 
     def set_exact_reductions(self, enable=True):
-        """2-D: serial reference-order dot products (bit-identical solves)."""
+        """Reference-order mode: serial dots (2-D), plus Eigen-order LL^T solves and
+        unfused updates (1-D, pcg1d_exact_kernel); bit-identical solves."""
         self._c(load().vqpc_set_exact_reductions(self.h, 1 if enable else 0))
 
     def factor_centroids(self):
