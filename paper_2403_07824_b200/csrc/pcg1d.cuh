@@ -429,7 +429,10 @@ __global__ void __launch_bounds__(T, MINB) pcg1d_kernel(const Pcg1dParams prm) {
     const double bb = (bbq[0] + bbq[1]) + (bbq[2] + bbq[3]);
     const int max_iter = prm.max_iter_arr ? prm.max_iter_arr[gs] : (prm.max_iter < 0 ? 10 * n : prm.max_iter);
 
-    double rz = 0.0, norm_b = 0.0, rel_rec = 0.0;
+    double rz = 0.0, norm_b = 0.0;
+    double rz_inv = 0.0;  // RN(1 / rz): beta = rz_next / rz by Markstein's correction (exact quotient)
+    double rr_hi = 0.0;   // rr above this => rel >= eps for certain (see below)
+    double rr_rec = 0.0;  // |b - A x|^2 of the last completed iteration (J of them)
     int J = 0;
     uint8_t st = VQPC_S_MAX_ITER;
     double rr_loc = 0.0;
@@ -483,7 +486,10 @@ __global__ void __launch_bounds__(T, MINB) pcg1d_kernel(const Pcg1dParams prm) {
       }
       // the relative true residual decides convergence; its sqrt and division
       // overlap sweep 2, and the (warp-uniform) exit is taken after it
-      const double rel = j > 0 ? sqrt(tree_sum<NWT>(S.red[1])) / norm_b : 0.0;
+      // |b - A x|^2 of this iteration; the exact rel = sqrt(rr)/|b| (solver.cpp:229) is
+      // only evaluated when rr is within 1e-9 of the threshold (eps |b|)^2 or at the
+      // exit, so its sqrt/division chain leaves the critical path of most iterations
+      const double rr = tree_sum<NWT>(S.red[1]);
       // ================= sweep 2 (ascending): barrier 3 =====================
       {
         double v[4];
@@ -526,8 +532,10 @@ __global__ void __launch_bounds__(T, MINB) pcg1d_kernel(const Pcg1dParams prm) {
       }
       if (j > 0) {
         J = j;
-        rel_rec = rel;
-        if (rel < prm.eps) {
+        rr_rec = rr;
+        // rr > rr_hi >= (eps |b|)^2 (1 + 0.9e-9) implies RN(RN(sqrt(rr)) / |b|) >= eps:
+        // the comparison's outcome is decided without evaluating rel (NaN takes the exact path)
+        if (!(rr > rr_hi) && sqrt(rr) / norm_b < prm.eps) {
           st = VQPC_S_CONVERGED;
           break;
         }
@@ -569,6 +577,7 @@ __global__ void __launch_bounds__(T, MINB) pcg1d_kernel(const Pcg1dParams prm) {
           break;
         }
         rz = rz_next;
+        rr_hi = (prm.eps * norm_b) * (prm.eps * norm_b) * (1.0 + 1e-9);
 #pragma unroll
         for (int i = 0; i < R; ++i) p[i] = wz[i];
         p_left = zl_left;
@@ -578,7 +587,18 @@ __global__ void __launch_bounds__(T, MINB) pcg1d_kernel(const Pcg1dParams prm) {
           st = VQPC_S_BREAKDOWN;
           break;
         }
-        const double beta = rz_next / rz;
+        // beta = RN(rz_next / rz): q0 = RN(a y), e = a - b q0 (exact), RN(q0 + e y) with
+        // y = RN(1/b) is the correctly rounded quotient (Markstein) as long as nothing
+        // under- or overflows; y was formed off the critical path, so only three dependent
+        // operations remain here. Stagnating samples drive rz towards the subnormal range:
+        // there (warp-uniform, rare) the IEEE division is used directly.
+        double beta;
+        if (rz > 1e-150 && rz < 1e150 && rz_next > 1e-150 && rz_next < 1e150) {
+          const double q0 = rz_next * rz_inv;
+          beta = fma(fma(-rz, q0, rz_next), rz_inv, q0);
+        } else {
+          beta = rz_next / rz;
+        }
         rz = rz_next;
 #pragma unroll
         for (int i = 0; i < R; ++i) p[i] = fma(beta, p[i], wz[i]);
@@ -596,6 +616,7 @@ __global__ void __launch_bounds__(T, MINB) pcg1d_kernel(const Pcg1dParams prm) {
         const double part = gwarp == NWT - 1 ? apply_rows<R, T, true>(p, p_left, p_right, ct, c_halo, j0, n, wz)
                                              : apply_rows<R, T, false>(p, p_left, p_right, ct, c_halo, j0, n, wz);
         const double a = warp_allsum(part);
+        rz_inv = __drcp_rn(rz);  // overlaps the reduction chain (used by next iteration's beta)
         if (lane == 0) send(S.red[0], gwarp, a, 0);
         xchg(0, NW * 8);  // barrier 1
         P1D_MARK(0);  // p update, A p, p.Ap
@@ -620,7 +641,7 @@ __global__ void __launch_bounds__(T, MINB) pcg1d_kernel(const Pcg1dParams prm) {
 
     if (rank == 0 && tid == 0) {
       prm.iters[gs] = J;
-      prm.rel[gs] = rel_rec;
+      prm.rel[gs] = J > 0 ? sqrt(rr_rec) / norm_b : 0.0;  // the record of iteration J
       prm.status[gs] = st;
     }
     if (prm.x_out) {
