@@ -162,6 +162,14 @@ struct Timed {
   }
 };
 
+// Diagnostics / determinism tests: VQPC_MAX_GROUPS=k caps the
+// persistent PCG grids at k concurrently resident samples (CTAs or clusters).
+int64_t cap_groups(int64_t g) {
+  const char* env = std::getenv("VQPC_MAX_GROUPS");  // read per launch (tests set it mid-process)
+  const int64_t cap = env ? std::atoll(env) : 0;
+  return cap > 0 ? std::min(g, cap) : g;
+}
+
 // ---- pcg variant table: rows per thread R, threads T (n <= R*T) ------------
 using PcgFn = void (*)(const Pcg1dParams);
 struct PcgVariant {
@@ -305,7 +313,7 @@ void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P2_DSMEM)));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P2_T, P2_DSMEM));
   if (per_sm < 1) throw ApiError{VQPC_CUDA_ERROR, "pcg2d kernel does not fit on an SM"};
-  const int64_t blocks = std::min<int64_t>(B, static_cast<int64_t>(per_sm) * c->sm_count);
+  const int64_t blocks = cap_groups(std::min<int64_t>(B, static_cast<int64_t>(per_sm) * c->sm_count));
   c->work2.ensure(static_cast<size_t>(blocks) * P2_WORK * c->n);
   c->counter.ensure(1);
   CK(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->stream));
@@ -362,7 +370,7 @@ void run_pcg1d_exact(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint
   const size_t smem = sizeof(double) * n;
   CK(cudaFuncSetAttribute(pcg1d_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg1d_exact_kernel, PX_T, smem));
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(B, static_cast<int64_t>(per_sm) * c->sm_count));
+  const int64_t blocks = std::max<int64_t>(1, cap_groups(std::min<int64_t>(B, static_cast<int64_t>(per_sm) * c->sm_count)));
   c->work1x.ensure(static_cast<size_t>(blocks) * (6 * static_cast<size_t>(n) + 1));
   c->counter.ensure(1);
   CK(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->stream));
@@ -457,7 +465,7 @@ void run_pcg(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d_k
     groups = clusters;
   }
   if (groups < 1) throw ApiError{VQPC_CUDA_ERROR, "pcg kernel does not fit on the device"};
-  groups = std::min<int64_t>(B, groups);
+  groups = cap_groups(std::min<int64_t>(B, groups));
   cfg.gridDim = dim3(static_cast<unsigned>(groups * v->CL));
   // diagnostics (VQPC_TAIL=1): per-CTA busy span, to size the work-queue tail
   static const bool tail = getenv("VQPC_TAIL") != nullptr;

@@ -313,3 +313,19 @@ def test_1d_exact_mode_bit_identical(name, n_real):
         assert np.array_equal(out["x"], x[i]), i
     print(name, "exact mode: %d samples bit-identical, J mean %.2f, statuses %s" % (
         len(xi), it.mean(), np.bincount(st)))
+
+
+@pytest.mark.parametrize("name,n_real", [("C2", 512), ("C5", 96), ("C4s", 64)])
+def test_grid_size_does_not_change_results(name, n_real, monkeypatch):
+    """Appendix B.6: results are independent of the launch geometry — the
+    persistent PCG grid capped at 1, 7 or 37 resident samples (CTAs / clusters)
+    gives every per-sample record bit for bit."""
+    cfg, basis, cb, xi = setup_case(name, n_real)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    a = ctx.run_campaign(xi, cfg["eps"])
+    for cap in (1, 7, 37):
+        monkeypatch.setenv("VQPC_MAX_GROUPS", str(cap))
+        b = ctx.run_campaign(xi, cfg["eps"])
+        for k in ("labels", "iterations", "rel", "status", "n_p", "sum_j"):
+            assert np.array_equal(a[k], b[k]), (cap, k)
+    monkeypatch.delenv("VQPC_MAX_GROUPS")
