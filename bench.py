@@ -251,6 +251,55 @@ def roofline(cfg, prof, total_iters, B, steps, device):
             "algorithmic": what, "ms_per_launch": ms}
 
 
+def dgemm_peak(dev, n=8192, reps=3):
+    """cuBLAS DGEMM throughput on this device (TFLOP/s): the fp64 tensor-core
+    (DMMA) roof for the realisation contraction."""
+    import torch
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    torch.matmul(a, b)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        torch.matmul(a, b)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    return 2.0 * n ** 3 * reps / (e0.elapsed_time(e1) / 1e3) / 1e12
+
+
+def kernel_rooflines(cfg, prof, total_iters, B, K, steps, peaks):
+    """Achieved work rate and roofline fraction of every kernel kind of the step.
+
+    pcg: 1-D 31 n fp64 flops per iteration (fp64 FMA pipe) / 2-D 8 (2 N_nodes + 14 n)
+    bytes per iteration (HBM); realise: 2 N K flops per sample (DGEMM / DMMA roof);
+    assign: 3 P d exact fp64 operations per sample (fp64 pipe); bucket: 16 bytes per
+    sample per counting-sort pass (HBM; two passes: label, then predicted cost)."""
+    r = cfg["mesh_resolution"]
+    n = (r - 1) ** cfg["dim"]
+    npts = r if cfg["dim"] == 1 else (r + 1) ** 2
+    P, d = cfg["quantizer"]["P"], cfg["m"]
+    nsolve = min(B, cfg.get("solve_subset") or B)
+    work = {}
+    if cfg["dim"] == 1:
+        work["pcg"] = (31.0 * n * total_iters / 1e12, "TFLOP/s", "fp64")
+    else:
+        work["pcg"] = (8.0 * (2 * npts + 14 * n) * total_iters / 1e9, "GB/s", "hbm")
+    work["realise"] = (2.0 * npts * K * B / 1e12, "TFLOP/s", "dgemm")
+    work["assign"] = (3.0 * P * d * B / 1e12, "TFLOP/s", "fp64")
+    work["bucket"] = (2 * 16.0 * nsolve / 1e9, "GB/s", "hbm")
+    out = {}
+    for k, (amount, unit, roof) in work.items():
+        ms = prof.get(k, {}).get("ms", 0.0) / steps
+        if ms <= 0:
+            continue
+        achieved = amount / (ms / 1e3)
+        peak = peaks.get(roof)
+        out[k] = {"achieved": achieved, "unit": unit, "roof": roof, "peak": peak,
+                  "frac": achieved / peak if peak else None}
+    return out
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     from paper_2403_07824_b200 import campaign, lib
@@ -332,6 +381,11 @@ def run_ours(args, rank, world, local_rank):
     step_ms = ms_max / args.steps
     kernels = {k: {"ms_per_step": v["ms"] / args.steps, "share": (v["ms"] / args.steps) / step_ms if step_ms else 0,
                    "launches": v["launches"]} for k, v in prof.items()}
+    # per-kernel achieved work and roofline fraction (north star: "per-kernel
+    # achieved fraction of HBM / fp64 roofline"), SURVEY §8(d) work per unit
+    peaks = {"fp64": lib.fp64_peak(local_rank), "dgemm": dgemm_peak(dev), "hbm": measured_peaks().get("hbm_gbs")}
+    for k, r in kernel_rooflines(cfg, prof, total_iters, B, K, args.steps, peaks).items():
+        kernels[k].update(r)
 
     # e2e through the host-buffer C-ABI entry point (copies inside the timed region)
     e2e_times = []
@@ -367,6 +421,9 @@ def run_ours(args, rank, world, local_rank):
                 "total_pcg_iterations_per_gpu_step": total_iters,
                 "roofline": roof,
                 "kernels": kernels,
+                "peaks": {"fp64_fma_tflops": peaks["fp64"], "dgemm_tflops": peaks["dgemm"], "hbm_gbs": peaks["hbm"],
+                          "source": "fp64: vqpc_fp64_peak DFMA probe; dgemm: torch.matmul fp64 8192^3 (cuBLAS, "
+                                    "DMMA); hbm: MEASURED_PEAKS.json"},
                 "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                 "gpu_launches": int(launches),
                 "clocks": clk.summary(),

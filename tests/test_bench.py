@@ -75,6 +75,29 @@ def test_roofline_pcg1d_and_realise_fp64(monkeypatch):
     assert roof["achieved"] == pytest.approx(2.0 * cfg5["mesh_resolution"] * cfg5["n_kl"] * (1 << 14) / 0.1 / 1e12)
 
 
+def test_per_kernel_rooflines():
+    """Every kernel kind of the step gets its SURVEY §8(d) work rate and roof:
+    pcg (1-D fp64 / 2-D HBM), realise (DGEMM roof), assign (fp64), bucket (HBM)."""
+    from paper_2403_07824_b200 import campaign
+    b = _bench()
+    cfg = campaign.CONFIGS["C2"]
+    n, N, K, B = cfg["mesh_resolution"] - 1, cfg["mesh_resolution"], 73, 1 << 17
+    prof = {"pcg": {"ms": 3 * 600.0, "launches": 3}, "realise": {"ms": 3 * 5.0, "launches": 3},
+            "assign": {"ms": 3 * 0.05, "launches": 3}, "bucket": {"ms": 3 * 0.1, "launches": 6},
+            "other": {"ms": 0.3, "launches": 3}}
+    peaks = {"fp64": 33.5, "dgemm": 36.0, "hbm": 6536.4}
+    r = b.kernel_rooflines(cfg, prof, 10 ** 7, B, K, 3, peaks)
+    assert set(r) == {"pcg", "realise", "assign", "bucket"}
+    assert r["pcg"]["achieved"] == pytest.approx(31.0 * n * 1e7 / 0.6 / 1e12) and r["pcg"]["roof"] == "fp64"
+    assert r["realise"]["achieved"] == pytest.approx(2.0 * N * K * B / 0.005 / 1e12)
+    assert r["realise"]["frac"] == pytest.approx(r["realise"]["achieved"] / 36.0)
+    assert r["assign"]["achieved"] == pytest.approx(3.0 * 64 * 8 * B / 0.00005 / 1e12)
+    assert r["bucket"]["unit"] == "GB/s" and r["bucket"]["frac"] == pytest.approx(r["bucket"]["achieved"] / 6536.4)
+    c4 = campaign.CONFIGS["C4"]
+    r4 = b.kernel_rooflines(c4, prof, 10 ** 6, 8192, 100, 3, peaks)
+    assert r4["pcg"]["roof"] == "hbm" and r4["pcg"]["unit"] == "GB/s"
+
+
 def test_reference_arm_contract(monkeypatch, capsys):
     """--impl reference on rank != 0 exits without output; rank 0 prints the
     contract keys (timed on a tiny C1 sample through the oracle)."""
