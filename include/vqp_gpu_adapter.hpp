@@ -113,8 +113,9 @@ inline std::vector<int> assign_all(const Context& c, const SampleSet& xi) {
 // (driver.hpp:93-95) on the GPU. Per-sample failures that make the reference
 // throw (pcg-breakdown inside a worker) are reported as unconverged
 // records instead of aborting the process.
-inline SimulationReport run_campaign_with(const CampaignConfig& config, const CampaignArtifacts& artifacts,
-                                          const SampleSet& realizations, const GpuOptions& opt) {
+namespace detail {
+inline SimulationReport campaign(const CampaignConfig& config, const CampaignArtifacts& artifacts,
+                                 const SampleSet& realizations, const GpuOptions& opt, std::vector<double>* x) {
   Context c(artifacts, opt);
   const int64_t B = realizations.n;
   const int P = artifacts.codebook.P;
@@ -122,10 +123,18 @@ inline SimulationReport run_campaign_with(const CampaignConfig& config, const Ca
   std::vector<double> rel(B);
   std::vector<uint8_t> status(B);
   std::vector<int64_t> stats(4 * static_cast<size_t>(P)), summary(4);
-  check(vqpc_run_campaign_ex(c.ctx(), realizations.data.data(), B, realizations.m, config.eps, -1, opt.chunk,
-                             opt.solve_limit, labels.data(), iters.data(), rel.data(), status.data(), stats.data(),
-                             summary.data()),
-        c.ctx());
+  if (x) {
+    x->assign(static_cast<size_t>(B) * vqpc_unknowns(c.ctx()), 0.0);
+    check(vqpc_run_campaign_x(c.ctx(), realizations.data.data(), B, realizations.m, config.eps, -1, opt.chunk,
+                              opt.solve_limit, labels.data(), iters.data(), rel.data(), status.data(), stats.data(),
+                              summary.data(), x->data()),
+          c.ctx());
+  } else {
+    check(vqpc_run_campaign_ex(c.ctx(), realizations.data.data(), B, realizations.m, config.eps, -1, opt.chunk,
+                               opt.solve_limit, labels.data(), iters.data(), rel.data(), status.data(), stats.data(),
+                               summary.data()),
+          c.ctx());
+  }
   SimulationReport rep;
   rep.n_realizations = B;
   rep.assignments.assign(labels.begin(), labels.end());
@@ -154,6 +163,22 @@ inline SimulationReport run_campaign_with(const CampaignConfig& config, const Ca
     }
   }
   return rep;
+}
+}  // namespace detail
+
+inline SimulationReport run_campaign_with(const CampaignConfig& config, const CampaignArtifacts& artifacts,
+                                          const SampleSet& realizations, const GpuOptions& opt) {
+  return detail::campaign(config, artifacts, realizations, opt, nullptr);
+}
+
+// run_campaign_with plus the solutions the reference computes and discards
+// (driver.cpp:236-237; SURVEY §8b run_campaign_with_solutions): x is resized to
+// B x n, row i = the PCG iterate of realisation i at its exit (zeros for
+// realisations that were not solved).
+inline SimulationReport run_campaign_with_solutions(const CampaignConfig& config, const CampaignArtifacts& artifacts,
+                                                    const SampleSet& realizations, const GpuOptions& opt,
+                                                    std::vector<double>& x) {
+  return detail::campaign(config, artifacts, realizations, opt, &x);
 }
 
 }  // namespace vqp::gpu

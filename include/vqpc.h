@@ -171,6 +171,14 @@ int vqpc_run_campaign_ex_d(vqpc_ctx* ctx, const double* d_xi, int64_t B, int ld,
                            int64_t chunk, int64_t solve_limit, int32_t* d_labels, int32_t* d_iters,
                            double* d_final_rel, uint8_t* d_status, int64_t* d_stats, int64_t* d_summary);
 
+/* Same as vqpc_run_campaign_ex, also returning the solutions the reference
+ * computes and discards (driver.cpp:236-237, SURVEY §8b "run_campaign_with_
+ * solutions"): x_out is B x n host memory; row i receives x of realisation i
+ * (rows of samples that are not solved keep their input values). */
+int vqpc_run_campaign_x(vqpc_ctx* ctx, const double* xi, int64_t B, int ld, double eps, int max_iter,
+                        int64_t chunk, int64_t solve_limit, int32_t* labels, int32_t* iters,
+                        double* final_rel, uint8_t* status, int64_t* stats, int64_t* summary, double* x_out);
+
 /* ---- per-kernel device timing (CUDA events on the context's stream) ------
  * enable != 0 brackets every kernel launch with events; vqpc_profile_read
  * synchronises and returns, per kernel kind, the accumulated milliseconds and

@@ -559,7 +559,7 @@ int64_t kappa_ld(const vqpc_ctx* c) { return (c->pb.n_nodes + 1) & ~1; }
 // The full campaign on device-resident arrays (run_campaign_with semantics).
 void campaign_device(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, double eps, int max_iter, int64_t chunk,
                      int32_t* d_labels, int32_t* d_iters, double* d_rel, uint8_t* d_status, int64_t* d_stats,
-                     int64_t* d_summary, int64_t solve_limit = INT64_MAX) {
+                     int64_t* d_summary, int64_t solve_limit = INT64_MAX, double* d_x = nullptr) {
   if (!(eps > 0.0) || eps >= 1.0) throw ApiError{VQPC_INVALID_TOLERANCE, "invalid-tolerance"};
   if (ld < c->pb.n_kl) throw ApiError{VQPC_INVALID_ARGUMENT, "ld < n_kl"};
   if (!c->factored) throw ApiError{VQPC_INVALID_CONFIG, "vqpc_factor_centroids must precede solves"};
@@ -610,12 +610,12 @@ void campaign_device(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, double 
     }
     run_schedule(c, xi, ld, d_labels + c0, nb, root);
     run_pcg(c, kap, ldk, kfl, c->perm.p, d_labels + c0, nb, c0, eps, max_iter, nullptr, d_iters, d_rel, d_status,
-            nullptr, solve_limit);
+            d_x, solve_limit);
   }
   if (merge) {
     run_schedule(c, d_xi, ld, d_labels, nsolve, root);
     run_pcg(c, c->kappa.p, ldk, c->kflag.p, c->perm.p, d_labels, nsolve, 0, eps, max_iter, nullptr, d_iters,
-            d_rel, d_status, nullptr, solve_limit);
+            d_rel, d_status, d_x, solve_limit);
   }
   CK(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 4 * P, c->stream));
   CK(cudaMemsetAsync(d_summary, 0, sizeof(int64_t) * 4, c->stream));
@@ -1021,6 +1021,38 @@ int vqpc_run_campaign_ex(vqpc_ctx* c, const double* xi, int64_t B, int ld, doubl
     d2h(c, status, c->status.p, B);
     d2h(c, stats, c->stats.p, 4 * static_cast<size_t>(P));
     d2h(c, summary, c->stats.p + 4 * P, 4);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+// run_campaign_with plus the solutions the reference computes and discards
+// (driver.cpp:236-237): x_out row i = x of realisation i (n doubles; rows of
+// unsolved samples are left untouched).
+int vqpc_run_campaign_x(vqpc_ctx* c, const double* xi, int64_t B, int ld, double eps, int max_iter, int64_t chunk,
+                        int64_t solve_limit, int32_t* labels, int32_t* iters, double* final_rel, uint8_t* status,
+                        int64_t* stats, int64_t* summary, double* x_out) {
+  if (!c || !x_out) return VQPC_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    const int P = c->pb.P;
+    const int64_t Bm = std::max<int64_t>(B, 1);
+    c->xi.ensure(static_cast<size_t>(Bm) * ld);
+    c->labels.ensure(Bm);
+    c->iters.ensure(Bm);
+    c->rel.ensure(Bm);
+    c->status.ensure(Bm);
+    c->stats.ensure(4 * static_cast<size_t>(P) + 4);
+    c->x.ensure(static_cast<size_t>(Bm) * c->n);
+    h2d(c, c->xi.p, xi, static_cast<size_t>(B) * ld);
+    h2d(c, c->x.p, x_out, static_cast<size_t>(B) * c->n);  // untouched rows keep the caller's values
+    campaign_device(c, c->xi.p, B, ld, eps, max_iter, chunk, c->labels.p, c->iters.p, c->rel.p, c->status.p,
+                    c->stats.p, c->stats.p + 4 * P, solve_limit < 0 ? INT64_MAX : solve_limit, c->x.p);
+    d2h(c, labels, c->labels.p, B);
+    d2h(c, iters, c->iters.p, B);
+    d2h(c, final_rel, c->rel.p, B);
+    d2h(c, status, c->status.p, B);
+    d2h(c, stats, c->stats.p, 4 * static_cast<size_t>(P));
+    d2h(c, summary, c->stats.p + 4 * P, 4);
+    d2h(c, x_out, c->x.p, static_cast<size_t>(B) * c->n);
     CK(cudaStreamSynchronize(c->stream));
   });
 }

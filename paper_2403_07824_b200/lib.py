@@ -67,6 +67,7 @@ def load():
             "vqpc_run_campaign_d": (I, [VP, VP, I64, I, D, I, I64, VP, VP, VP, VP, VP, VP]),
             "vqpc_run_campaign_ex": (I, [VP, VP, I64, I, D, I, I64, I64, VP, VP, VP, VP, VP, VP]),
             "vqpc_run_campaign_ex_d": (I, [VP, VP, I64, I, D, I, I64, I64, VP, VP, VP, VP, VP, VP]),
+            "vqpc_run_campaign_x": (I, [VP, VP, I64, I, D, I, I64, I64, VP, VP, VP, VP, VP, VP, VP]),
             "vqpc_kmeans": (I, [I, VP, I, I, VP, I, I, U64, I, D, VP, VP, C.POINTER(C.c_int)]),
             "vqpc_draw_standard_normal": (I, [I64, I, U64, I64, VP, I]),
             "vqpc_profile": (I, [VP, I]),
@@ -267,9 +268,11 @@ class Context:
                                         _p(st), _p(x)))
         return it, rel, st, x
 
-    def run_campaign(self, xi, eps, max_iter=-1, chunk=0, solve_limit=-1):
+    def run_campaign(self, xi, eps, max_iter=-1, chunk=0, solve_limit=-1, want_x=False):
         """run_campaign_with (driver.cpp:193-281) on host arrays (copies included);
-        solve_limit >= 0 solves only the first solve_limit samples (C5)."""
+        solve_limit >= 0 solves only the first solve_limit samples (C5);
+        want_x also returns the solutions the reference discards (driver.cpp:236-237)
+        as res["x"] (B x n; rows of unsolved samples are NaN)."""
         xi = f64(xi)
         B, ld = xi.shape
         P = self.P
@@ -279,9 +282,15 @@ class Context:
         st = np.empty(B, np.uint8)
         stats = np.empty(4 * P, np.int64)
         summary = np.empty(4, np.int64)
-        self._c(load().vqpc_run_campaign_ex(self.h, _p(xi), B, ld, eps, max_iter, chunk, solve_limit, _p(labels),
-                                            _p(it), _p(rel), _p(st), _p(stats), _p(summary)))
-        return dict(labels=labels, iterations=it, rel=rel, status=st, n_p=stats[:P], sum_j=stats[P:2 * P],
+        x = None
+        if want_x:
+            x = np.full((B, self.n), np.nan)
+            self._c(load().vqpc_run_campaign_x(self.h, _p(xi), B, ld, eps, max_iter, chunk, solve_limit, _p(labels),
+                                               _p(it), _p(rel), _p(st), _p(stats), _p(summary), _p(x)))
+        else:
+            self._c(load().vqpc_run_campaign_ex(self.h, _p(xi), B, ld, eps, max_iter, chunk, solve_limit,
+                                                _p(labels), _p(it), _p(rel), _p(st), _p(stats), _p(summary)))
+        return dict(x=x, labels=labels, iterations=it, rel=rel, status=st, n_p=stats[:P], sum_j=stats[P:2 * P],
                     conv_count=stats[2 * P:3 * P], conv_sum=stats[3 * P:], total_iterations=int(summary[0]),
                     unconverged=int(summary[1]), conv_total=int(summary[2]), conv_sum_total=int(summary[3]))
 

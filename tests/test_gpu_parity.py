@@ -329,3 +329,27 @@ def test_grid_size_does_not_change_results(name, n_real, monkeypatch):
         for k in ("labels", "iterations", "rel", "status", "n_p", "sum_j"):
             assert np.array_equal(a[k], b[k]), (cap, k)
     monkeypatch.delenv("VQPC_MAX_GROUPS")
+
+
+@pytest.mark.parametrize("name,n_real,limit", [("C2", 96, -1), ("C5", 40, 24), ("C4s", 24, -1)])
+def test_campaign_with_solutions(name, n_real, limit):
+    """SURVEY §8b run_campaign_with_solutions: the campaign returns the x the
+    reference discards (driver.cpp:236-237); it equals the per-batch solve's x bit
+    for bit (same kernel, same queue-independent arithmetic), rows beyond the
+    solve subset stay untouched, and in reference-order mode it is the oracle's x."""
+    cfg, basis, cb, xi = setup_case(name, n_real)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    res = ctx.run_campaign(xi, cfg["eps"], solve_limit=limit, want_x=True)
+    ns = n_real if limit < 0 else limit
+    assert np.isnan(res["x"][ns:]).all() and not np.isnan(res["x"][:ns]).any()
+    it, rel, st, x = ctx.solve_batch(xi[:ns], res["labels"][:ns], cfg["eps"], want_x=True)
+    assert np.array_equal(it, res["iterations"][:ns]) and np.array_equal(x, res["x"][:ns])
+    if cfg["dim"] == 1:
+        ctx.set_exact_reductions(True)
+        kc = ctx.centroid_coefficients()
+        kap, _ = ctx.realise(xi[:4])
+        r2 = ctx.run_campaign(xi[:4], cfg["eps"], max_iter=400, want_x=True)
+        pset = oracle.PreconditionerSet.from_coefficients(1, cfg["mesh_resolution"], "cholesky", kc)
+        for i in range(4):
+            out = pset.pcg(int(r2["labels"][i]), kap[i], cfg["eps"], max_iter=400)
+            assert out["iterations"] == r2["iterations"][i] and np.array_equal(out["x"], r2["x"][i]), i
