@@ -408,7 +408,8 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu:
         n_cpu = args.cpu_samples or cpu_sample_size(cfg)
         cpu = cpu_baseline(cfg, arts, n_cpu)
-        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cpu = {**{k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+               "stage_seconds": cpu.get("stage_seconds")}  # assign / build / solve / reduce
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
