@@ -60,9 +60,10 @@
 // Dead rows j >= n: n_j = 1/u_j^2 = 0 (so z_j = p_j = x_j = 0) and n_{n-1} = 0.
 // Shared memory holds the conductances c_j for j <= n (c_n is the true right
 // conductance of row n-1, so d_{n-1} = c_{n-1} + c_n needs no special case;
-// its coupling term multiplies the dead p_n = 0) and 0 beyond. Only the last
-// warp can own dead rows, so A p and b - A x take a masked code path there
-// behind a warp-uniform branch (row n would otherwise see c_n).
+// its coupling term multiplies the dead p_n = 0) and 0 beyond. Warps that own
+// dead rows (the last one for n = 2^k - 1; up to all but the first for other n)
+// take a masked code path for A p and b - A x behind a warp-uniform branch (row
+// n would otherwise see c_n, and every dead row would add b_j = h to |b - A x|).
 #pragma once
 #include <cooperative_groups.h>
 
@@ -276,6 +277,8 @@ __global__ void __launch_bounds__(T, MINB) pcg1d_kernel(const Pcg1dParams prm) {
   const int rank = CL == 1 ? 0 : static_cast<int>(cg::this_cluster().block_rank());
   const int gwarp = rank * NW + warp;  // warp index within the sample
   const int j0 = (rank * T + tid) * R;  // first row of this thread
+  // this warp owns rows >= n (warp-uniform): only then the masked row paths run
+  const bool dead_warp = (gwarp + 1) * 32 * R > prm.n;
   // peer CTA's shared struct (CL == 2); same layout at the same offset
   Sh* peer = &S;
   if constexpr (CL == 2) peer = cg::this_cluster().map_shared_rank(&S, rank ^ 1);
@@ -612,8 +615,8 @@ __global__ void __launch_bounds__(T, MINB) pcg1d_kernel(const Pcg1dParams prm) {
         break;
       }
       {
-        // dead rows (j >= n) only exist in the last warp: warp-uniform masked path
-        const double part = gwarp == NWT - 1 ? apply_rows<R, T, true>(p, p_left, p_right, ct, c_halo, j0, n, wz)
+        // dead rows (j >= n) take a warp-uniform masked path (row n would see c_n)
+        const double part = dead_warp ? apply_rows<R, T, true>(p, p_left, p_right, ct, c_halo, j0, n, wz)
                                              : apply_rows<R, T, false>(p, p_left, p_right, ct, c_halo, j0, n, wz);
         const double a = warp_allsum(part);
         rz_inv = __drcp_rn(rz);  // overlaps the reduction chain (used by next iteration's beta)
@@ -634,8 +637,8 @@ __global__ void __launch_bounds__(T, MINB) pcg1d_kernel(const Pcg1dParams prm) {
       }
       x_left = fma(alpha, p_left, x_left);
       x_right = fma(alpha, p_right, x_right);
-      // true residual b - A x; dead rows (b_j = 0) only exist in the last warp
-      rr_loc = gwarp == NWT - 1 ? true_residual<R, T, true>(x, x_left, x_right, ct, c_halo, prm.h, j0, n)
+      // true residual b - A x; dead rows (b_j = 0) are masked
+      rr_loc = dead_warp ? true_residual<R, T, true>(x, x_left, x_right, ct, c_halo, prm.h, j0, n)
                               : true_residual<R, T, false>(x, x_left, x_right, ct, c_halo, prm.h, j0, n);
     }
 

@@ -353,3 +353,35 @@ def test_campaign_with_solutions(name, n_real, limit):
         for i in range(4):
             out = pset.pcg(int(r2["labels"][i]), kap[i], cfg["eps"], max_iter=400)
             assert out["iterations"] == r2["iterations"][i] and np.array_equal(out["x"], r2["x"][i]), i
+
+
+@pytest.mark.parametrize("N", [600, 1100, 3000, 5000])
+def test_1d_sizes_with_dead_rows_in_several_warps(N):
+    """Meshes whose n is not 2^k - 1 leave padded (dead) rows in several warps
+    of the thread layout (N = 600: two warps of the 8 x 128 layout; 1100, 3000:
+    two and three warps; 5000: six warps across the 2-CTA cluster). At a fixed
+    iteration count the GPU's iterate and true-residual record match the oracle
+    to rounding, and campaign statuses agree."""
+    cfg = campaign.scaled(campaign.CONFIGS["C1"], mesh_resolution=N, n_realizations=48)
+    basis = campaign.load_or_build_basis(cfg)
+    cb = campaign.load_or_build_codebook(cfg, basis, kmeans_fn=oracle.kmeans, draw_fn=oracle.draw_standard_normal)
+    K = basis["eigenvalues"].size
+    xi = oracle.draw_standard_normal(48, K, cfg["master_seed"])
+    ocb = oracle_codebook(cb)
+    labels = oracle.assign(ocb, xi)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    assert np.array_equal(ctx.assign(xi), labels)
+    kc = ctx.centroid_coefficients()
+    kap, _ = ctx.realise(xi)
+    pset = oracle.PreconditionerSet.from_coefficients(1, N, "cholesky", kc)
+    it, rel, st, x = ctx.solve_batch(xi, labels, 1e-300, max_iter=12, want_x=True)
+    assert (it == 12).all()
+    for i in range(len(xi)):
+        out = pset.pcg(int(labels[i]), kap[i, :N], 1e-300, max_iter=12)
+        assert abs(out["rel"] - rel[i]) <= 1e-6 * out["rel"], (i, out["rel"], rel[i])  # (the bug: 1e2-1e3x)
+        assert np.linalg.norm(out["x"] - x[i]) <= 1e-10 * np.linalg.norm(out["x"]), i
+    res = ctx.run_campaign(xi, cfg["eps"])
+    ref = oracle.run_campaign(1, N, "cholesky", ocb, basis["eigenvalues"], basis["eigenvectors"], xi, cfg["eps"])
+    assert np.mean(res["status"] == ref["status"]) >= 0.95
+    both = (res["status"] == 0) & (ref["status"] == 0)
+    assert np.abs(res["iterations"][both].astype(int) - ref["iterations"][both]).max() <= 4
