@@ -285,6 +285,9 @@ struct Pcg2dParams {
   double* x_out;            // nullable, natural interior order
   int exact;                // 1: dot products summed serially in natural order (reference bits)
   const int* gmap;          // per wavefront address: level | (iy << 16)
+  const double* bvec;       // per wavefront address: b_i = area_sum_i / 3 when the mesh's b is not
+                            // uniform (h = 1/r inexact: every triangle area rounds differently); null:
+                            // b is the same for every node (r a power of two, e.g. C4) and read once
 };
 
 constexpr int P2_WORK = 11;  // per-CTA scratch vectors: d, w, s, x[2], r, p[2], y, z, prod
@@ -450,7 +453,7 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
         As[a] = rc.s;
         Xb[0][a] = 0.0;
         Rv[a] = rc.b;
-        if (t == 0 && l == 0) s_bval = rc.b;  // b_i = area_sum / 3: the same for every interior node
+        if (t == 0 && l == 0) s_bval = rc.b;  // b_i = area_sum / 3: uniform unless prm.bvec is set
         bb_loc = fma(rc.b, rc.b, bb_loc);
         if (exact) Prod[nat(l)] = __dmul_rn(rc.b, rc.b);
       }
@@ -684,13 +687,15 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
           for (int k = 0; k < P2_SD; ++k) flat_issue(k, Pv, Xo, Rv);
           double cs = 0.0, cw = 0.0, cd = 0.0, cr = 0.0;
           int clv = 0;
+          double cb = bval;  // b of this thread's address in the chunk being loaded
           for (int k = 0; k <= NC; ++k) {
-            const double ps = cs, pw = cw, pd = cd, pr = cr;
+            const double ps = cs, pw = cw, pd = cd, pr = cr, pb = cb;
             const int plv = clv;
             if (k < NC) {
               cp_wait<P2_SD - 1>();
               const int a = k * P2_T + t;
               if (a < n) {
+                if (prm.bvec) cb = __ldg(prm.bvec + a);  // consumed one chunk later (latency hidden)
                 const double pvv = *RAW(k, 0);
                 const double xn = __dadd_rn(*RAW(k, 1), __dmul_rn(alpha, pvv));
                 cr = *RAW(k, 2);
@@ -715,7 +720,7 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
                                           xv(0, b.nn));
               const double ax = row_apply(ps, pw, pd, aE, aN, xv(1, b.s), xv(1, b.w), XCH(1, a), xv(1, b.e),
                                           xv(1, b.nn));
-              const double rt = __dsub_rn(bval, ax);
+              const double rt = __dsub_rn(pb, ax);
               rr = fma(rt, rt, rr);
               if (exact) Prod[b.iy * g.m + b.ix] = __dmul_rn(rt, rt);
               Rv[a] = __dsub_rn(pr, __dmul_rn(alpha, ap));
@@ -766,6 +771,16 @@ __global__ void __launch_bounds__(P2_T) build_gmap_kernel(const Grid2D g, int* g
   for (int l = blockIdx.x; l < g.L; l += gridDim.x) {
     const int lo = tab.lo[l], hi = lvl_hi(l, g.m);
     for (int iy = lo + threadIdx.x; iy <= hi; iy += blockDim.x) gmap[tab.off[l] + iy - lo] = l | (iy << 16);
+  }
+}
+
+// per wavefront address: b_i = area_sum_i / 3 with the assembly's own operations
+// (assemble_row; kappa does not enter b). Used when the mesh's b is not uniform.
+__global__ void __launch_bounds__(P2_T) build_bvec_kernel(const Grid2D g, const double* kappa_any, const int* gmap,
+                                                          double* bvec) {
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < g.n; a += gridDim.x * blockDim.x) {
+    const int lv = gmap[a], l = lv & 0xffff, iy = lv >> 16;
+    bvec[a] = assemble_row(kappa_any, g, l - iy, iy).b;
   }
 }
 

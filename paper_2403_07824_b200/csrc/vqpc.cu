@@ -98,6 +98,8 @@ struct vqpc_ctx {
   Grid2D g2{};
   DBuf<double> fac2, work2;
   DBuf<int> gmap;
+  DBuf<double> bvec2;  // per-node right-hand side when it is not uniform (see pcg2d.cuh)
+  bool b2_checked = false, b2_uniform = true;
   int exact = 0;  // reference-order mode: serial dot products (2-D); 1-D: pcg1d_exact_kernel
   DBuf<double2> fac_lu;  // 1-D reference-order mode: P x NP {l_j, u_j}, built on first use
   bool have_lu = false;
@@ -344,6 +346,17 @@ void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d
     launch_check(c);
   }
   prm.gmap = c->gmap.p;
+  if (!c->b2_checked) {  // is b_i = area_sum_i / 3 the same for every node? (yes when h = 1/r is exact)
+    c->bvec2.ensure(c->n);
+    build_bvec_kernel<<<64, P2_T, 0, c->stream>>>(c->g2, c->kappa_c.p, c->gmap.p, c->bvec2.p);
+    launch_check(c);
+    std::vector<double> hb(c->n);
+    CK(cudaMemcpyAsync(hb.data(), c->bvec2.p, sizeof(double) * c->n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->b2_uniform = std::all_of(hb.begin(), hb.end(), [&](double v) { return v == hb[0]; });
+    c->b2_checked = true;
+  }
+  prm.bvec = c->b2_uniform ? nullptr : c->bvec2.p;
   Timed tm(c, VQPC_K_PCG);
   kern<<<static_cast<unsigned>(blocks), P2_T, P2_DSMEM, c->stream>>>(prm);
   launch_check(c);
@@ -742,6 +755,7 @@ void vqpc_ctx_destroy(vqpc_ctx* c) {
   c->counter.release();
   c->err.release();
   c->gmap.release();
+  c->bvec2.release();
   for (auto& r : c->recs) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);

@@ -100,9 +100,17 @@ def build_kl_basis_2d(r: int, sigma2: float, ell: float, n_kl: int, cutoff: bool
         Y = sigma2 * (C1 @ V @ C1.T)
         return sm * Y.reshape(-1)
 
-    op = LinearOperator((nn, nn), matvec=mv, dtype=np.float64)
-    rng = np.random.default_rng(12345)
-    w, v = eigsh(op, k=n_kl, which="LA", tol=tol, v0=rng.standard_normal(nn), ncv=min(nn, max(2 * n_kl + 1, n_kl + 64)))
+    if n_kl >= nn - 1:
+        # tiny meshes (n_kl modes are all of them): the dense W (Lanczos needs k < N)
+        import scipy.linalg as sl
+        W = (sm[:, None] * (sigma2 * np.kron(C1, C1))) * sm[None, :]
+        k = min(n_kl, nn)
+        w, v = sl.eigh(W, subset_by_index=[nn - k, nn - 1])
+    else:
+        op = LinearOperator((nn, nn), matvec=mv, dtype=np.float64)
+        rng = np.random.default_rng(12345)
+        w, v = eigsh(op, k=n_kl, which="LA", tol=tol, v0=rng.standard_normal(nn),
+                     ncv=min(nn, max(2 * n_kl + 1, n_kl + 64)))
     order = np.argsort(w)[::-1]
     lam, phi = _finish(w[order], v[:, order], sm, n_kl, cutoff)
     return dict(eigenvalues=lam, eigenvectors=phi, mass=mass, total_variance=sigma2 * float(mass.sum()),

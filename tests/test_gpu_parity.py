@@ -385,3 +385,52 @@ def test_1d_sizes_with_dead_rows_in_several_warps(N):
     assert np.mean(res["status"] == ref["status"]) >= 0.95
     both = (res["status"] == 0) & (ref["status"] == 0)
     assert np.abs(res["iterations"][both].astype(int) - ref["iterations"][both]).max() <= 4
+
+
+@pytest.mark.parametrize("N", [2, 3, 65])
+def test_1d_tiny_meshes(N):
+    """Degenerate sizes: n = 1, 2, 64 unknowns (almost every row of the thread
+    layout is padding). Reference-order mode is bit-identical to the oracle; the
+    fast kernel agrees in status and to rounding in J."""
+    nkl = min(50, N)
+    cfg = campaign.scaled(campaign.CONFIGS["C1"], mesh_resolution=N, n_realizations=24, n_kl=nkl, m=min(4, nkl))
+    basis = campaign.load_or_build_basis(cfg)
+    cb = campaign.load_or_build_codebook(cfg, basis, kmeans_fn=oracle.kmeans, draw_fn=oracle.draw_standard_normal)
+    xi = oracle.draw_standard_normal(24, basis["eigenvalues"].size, cfg["master_seed"])
+    ocb = oracle_codebook(cb)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    res = ctx.run_campaign(xi, cfg["eps"])
+    ref = oracle.run_campaign(1, N, "cholesky", ocb, basis["eigenvalues"], basis["eigenvectors"], xi, cfg["eps"])
+    assert np.array_equal(res["labels"], ref["labels"])
+    assert np.array_equal(res["status"], ref["status"])
+    assert np.abs(res["iterations"].astype(int) - ref["iterations"]).max() <= 1
+    ctx.set_exact_reductions(True)
+    kc = ctx.centroid_coefficients()
+    kap, _ = ctx.realise(xi)
+    pset = oracle.PreconditionerSet.from_coefficients(1, N, "cholesky", kc)
+    it, rel, st, x = ctx.solve_batch(xi, res["labels"], cfg["eps"], want_x=True)
+    for i in range(len(xi)):
+        out = pset.pcg(int(res["labels"][i]), kap[i, :N], cfg["eps"])
+        assert out["iterations"] == it[i] and out["rel"] == rel[i] and np.array_equal(out["x"], x[i]), i
+
+
+@pytest.mark.parametrize("r", [4, 17, 100])
+def test_2d_other_mesh_sizes_exact_mode(r):
+    """2-D meshes other than C4's (generic kernel instantiation, odd and tiny m):
+    reference-order mode is bit-identical to the oracle fed the same kappa."""
+    cfg = campaign.scaled(campaign.CONFIGS["C4"], mesh_resolution=r, n_realizations=12, ns=4000)
+    basis = campaign.load_or_build_basis(cfg)
+    cb = campaign.load_or_build_codebook(cfg, basis, kmeans_fn=oracle.kmeans, draw_fn=oracle.draw_standard_normal)
+    xi = oracle.draw_standard_normal(12, basis["eigenvalues"].size, cfg["master_seed"])
+    ocb = oracle_codebook(cb)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    ctx.set_exact_reductions(True)
+    kc = ctx.centroid_coefficients()
+    labels = oracle.assign(ocb, xi)
+    kap, _ = ctx.realise(xi)
+    pset = oracle.PreconditionerSet.from_coefficients(2, r, "ic0", kc)
+    it, rel, st, x = ctx.solve_batch(xi, labels, cfg["eps"], want_x=True)
+    for i in range(len(xi)):
+        out = pset.pcg(int(labels[i]), kap[i], cfg["eps"])
+        assert out["iterations"] == it[i] and out["status"] == st[i] and out["rel"] == rel[i], i
+        assert np.array_equal(out["x"], x[i]), i
