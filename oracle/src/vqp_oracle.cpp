@@ -225,6 +225,40 @@ static void check_coefficient(const double* kappa, int nn) {
     if (!(kappa[i] > 0.0) || !std::isfinite(kappa[i])) throw Err(INVALID_COEFFICIENT);
 }
 
+// The reference's SparseBuilder (fem.cpp:177-211) operation for operation: every
+// contribution is appended in insertion order, each row is ordered with std::sort
+// on the column (not stable: for rows of more than 16 entries libstdc++'s
+// introsort permutes equal columns), and duplicates are summed in that order,
+// the first one initialising the entry. Used for the 2-D assembly so the CSR
+// values are bit-identical to the reference's (same standard library).
+struct RefSparseBuilder {
+  int n;
+  std::vector<std::vector<std::pair<int, double>>> rows;
+  explicit RefSparseBuilder(int n_) : n(n_), rows(n_) {}
+  void add(int i, int j, double v) { rows[i].emplace_back(j, v); }
+  Csr finish() {
+    Csr A;
+    A.n = n;
+    A.row_ptr.assign(n + 1, 0);
+    for (int i = 0; i < n; ++i) {
+      auto row = rows[i];
+      std::sort(row.begin(), row.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+      int last = -1;
+      for (const auto& [j, v] : row) {
+        if (j != last) {
+          A.col.push_back(j);
+          A.val.push_back(v);
+          last = j;
+        } else {
+          A.val.back() += v;
+        }
+      }
+      A.row_ptr[i + 1] = static_cast<int>(A.col.size());
+    }
+    return A;
+  }
+};
+
 // 1-D model: N elements of length h = 1/N, coefficient per
 // element (midpoint value), unknowns at interior nodes 1..N-1 numbered 0..N-2.
 static System assemble_1d(int N, const double* kappa) {
@@ -264,7 +298,7 @@ static System assemble_2d(int r, const double* kappa) {
       if (ix > 0 && iy > 0 && ix < r && iy < r) interior[iy * side + ix] = n++;
   auto X = [&](int id) { return (id % side) * h; };
   auto Y = [&](int id) { return (id / side) * h; };
-  RowAccumulator acc(n);
+  RefSparseBuilder acc(n);
   std::vector<double> area_sum(nn, 0.0);
   for (int cy = 0; cy < r; ++cy)
     for (int cx = 0; cx < r; ++cx) {

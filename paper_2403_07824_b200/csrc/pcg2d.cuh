@@ -43,6 +43,12 @@ constexpr int P2_FAC = 4;            // factor vectors per centroid: D, aW, aS, 
 constexpr int P2_MAXL = 2 * P2_T;    // max levels (2m - 1 <= 511)
 
 struct Grid2D {
+  // order in which the reference's SparseBuilder sums a row's six diagonal
+  // contributions (fem.cpp:177-211: std::sort by column, then duplicates summed
+  // in sorted order), per row pattern W | E << 1 | S << 2 | N << 3 of present
+  // neighbours; entry k = index (in triangle order) of the k-th term. Filled on
+  // the host with the same std::sort (diag_orders in vqpc.cu).
+  unsigned char dperm[16][6];
   int r;       // mesh resolution
   int m;       // interior nodes per row (r - 1)
   int n;       // m * m
@@ -98,39 +104,44 @@ __device__ inline void cell_tri(int cx, int cy, int which, int X[3], int Y[3]) {
 __device__ inline RowCoef assemble_row(const double* kappa, const Grid2D g, int ix, int iy) {
   const int side = g.r + 1, X = ix + 1, Y = iy + 1;
   int tx[3], ty[3];
-  double area, diag, asum, e1, e2;
+  double area, asum, e1, e2, dt[6];  // dt: the six diagonal contributions in triangle order
   // 1) T1(X-1,Y-1): node is d (local 2)
   cell_tri(X - 1, Y - 1, 1, tx, ty);
-  diag = tri_entry(kappa, side, tx, ty, 2, 2, g.h, &area);
+  dt[0] = tri_entry(kappa, side, tx, ty, 2, 2, g.h, &area);
   asum = area;
   const double s1 = tri_entry(kappa, side, tx, ty, 2, 1, g.h, nullptr);  // S via T1(X-1,Y-1): (d, b)
   // 2) T2(X-1,Y-1): node is d (local 1)
   cell_tri(X - 1, Y - 1, 2, tx, ty);
-  diag = __dadd_rn(diag, tri_entry(kappa, side, tx, ty, 1, 1, g.h, &area));
+  dt[1] = tri_entry(kappa, side, tx, ty, 1, 1, g.h, &area);
   asum = __dadd_rn(asum, area);
   const double w1 = tri_entry(kappa, side, tx, ty, 1, 2, g.h, nullptr);  // W via T2(X-1,Y-1): (d, c)
   // 3) T2(X,Y-1): node is c (local 2)
   cell_tri(X, Y - 1, 2, tx, ty);
-  diag = __dadd_rn(diag, tri_entry(kappa, side, tx, ty, 2, 2, g.h, &area));
+  dt[2] = tri_entry(kappa, side, tx, ty, 2, 2, g.h, &area);
   asum = __dadd_rn(asum, area);
   const double s2 = tri_entry(kappa, side, tx, ty, 2, 0, g.h, nullptr);  // S via T2(X,Y-1): (c, a)
   e1 = tri_entry(kappa, side, tx, ty, 2, 1, g.h, nullptr);                // E via T2(X,Y-1): (c, d)
   // 4) T1(X-1,Y): node is b (local 1)
   cell_tri(X - 1, Y, 1, tx, ty);
-  diag = __dadd_rn(diag, tri_entry(kappa, side, tx, ty, 1, 1, g.h, &area));
+  dt[3] = tri_entry(kappa, side, tx, ty, 1, 1, g.h, &area);
   asum = __dadd_rn(asum, area);
   const double w2 = tri_entry(kappa, side, tx, ty, 1, 0, g.h, nullptr);  // W via T1(X-1,Y): (b, a)
   const double n1 = tri_entry(kappa, side, tx, ty, 1, 2, g.h, nullptr);  // N via T1(X-1,Y): (b, d)
   // 5) T1(X,Y): node is a (local 0)
   cell_tri(X, Y, 1, tx, ty);
-  diag = __dadd_rn(diag, tri_entry(kappa, side, tx, ty, 0, 0, g.h, &area));
+  dt[4] = tri_entry(kappa, side, tx, ty, 0, 0, g.h, &area);
   asum = __dadd_rn(asum, area);
   e2 = tri_entry(kappa, side, tx, ty, 0, 1, g.h, nullptr);  // E via T1(X,Y): (a, b)
   // 6) T2(X,Y): node is a (local 0)
   cell_tri(X, Y, 2, tx, ty);
-  diag = __dadd_rn(diag, tri_entry(kappa, side, tx, ty, 0, 0, g.h, &area));
+  dt[5] = tri_entry(kappa, side, tx, ty, 0, 0, g.h, &area);
   asum = __dadd_rn(asum, area);
   const double n2 = tri_entry(kappa, side, tx, ty, 0, 2, g.h, nullptr);  // N via T2(X,Y): (a, c)
+  // the diagonal in the reference's sorted-duplicate order for this row pattern
+  const int pat = (ix > 0 ? 1 : 0) | (ix < g.m - 1 ? 2 : 0) | (iy > 0 ? 4 : 0) | (iy < g.m - 1 ? 8 : 0);
+  double diag = dt[g.dperm[pat][0]];
+#pragma unroll
+  for (int k = 1; k < 6; ++k) diag = __dadd_rn(diag, dt[g.dperm[pat][k]]);
   RowCoef rc;
   rc.d = diag;
   rc.w = ix > 0 ? __dadd_rn(w1, w2) : 0.0;

@@ -172,6 +172,32 @@ int64_t cap_groups(int64_t g) {
   return cap > 0 ? std::min(g, cap) : g;
 }
 
+// Per row pattern of the structured 2-D mesh (neighbours W, E, S, N present),
+// the order in which the reference's SparseBuilder (fem.cpp:177-211) sums the six
+// diagonal contributions: the row's insertion sequence (triangles in mesh order,
+// vertices j = 0..2 each; assemble, fem.cpp:226-245) is ordered with the same
+// std::sort on the column, and the diagonal's terms are read off in sorted order.
+// Keys are column ranks SW < S < W < C < E < N < NE (the order of the true interior
+// indices for m >= 2), which std::sort treats exactly like the true columns.
+void diag_orders(unsigned char out[16][6]) {
+  enum { SW, S, W, C, E, N, NE };
+  // node C's six triangles in mesh order: T1, T2 of cell (X-1, Y-1), T2 of (X, Y-1),
+  // T1 of (X-1, Y), T1, T2 of (X, Y); their vertices in local order
+  static const int seq[18] = {SW, S, C, SW, C, W, S, E, C, W, C, N, C, E, NE, C, NE, N};
+  for (int pat = 0; pat < 16; ++pat) {
+    const bool hw = pat & 1, he = pat & 2, hs = pat & 4, hn = pat & 8;
+    const bool has[7] = {hw && hs, hs, hw, true, he, hn, he && hn};
+    std::vector<std::pair<int, double>> row;  // the reference's element type
+    int tag = 0;
+    for (int q = 0; q < 18; ++q)
+      if (has[seq[q]]) row.emplace_back(seq[q], seq[q] == C ? static_cast<double>(tag++) : -1.0);
+    std::sort(row.begin(), row.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    int k = 0;
+    for (const auto& e : row)
+      if (e.first == C) out[pat][k++] = static_cast<unsigned char>(e.second);
+  }
+}
+
 // ---- pcg variant table: rows per thread R, threads T (n <= R*T) ------------
 using PcgFn = void (*)(const Pcg1dParams);
 struct PcgVariant {
@@ -699,6 +725,7 @@ int vqpc_ctx_create(const vqpc_problem* pb, vqpc_ctx** out) {
       c->g2.n = c->g2.m * c->g2.m;
       c->g2.L = 2 * c->g2.m - 1;
       c->g2.h = 1.0 / pb->size;
+      diag_orders(c->g2.dperm);
     }
     if (pb->dim == 1) {
       const PcgVariant* v = pick_pcg(c->n);
