@@ -124,4 +124,76 @@ static __global__ void __launch_bounds__(RL_THREADS) realise_kernel(const Realis
   }
 }
 
+// Reference-order realisation (vqpc_set_exact_reductions): h = lift(xi) as the
+// reference's k-outer AXPY (field.cpp:113-125) — h_i = 0; for each k with
+// w_k = sqrt(lambda_k) xi_k != 0: h_i += w_k * phi_ki, product and sum rounded
+// separately — on the CUDA cores, then kappa = exp(h) as in the DMMA kernel. h is
+// bit-identical to the reference's lift; kappa differs from a glibc exp by at most
+// CUDA exp's 1-ulp error. Same tiling as realise_kernel (64 samples x 128 points
+// per CTA); each thread owns 4 samples x 8 points.
+static __global__ void __launch_bounds__(RL_THREADS) realise_exact_kernel(const RealiseParams prm) {
+  __shared__ double sW[RL_BM * RL_WLD];
+  __shared__ double sP[RL_BK * RL_PLD];
+  const int tid = threadIdx.x;
+  const int ts = tid >> 4, tp = tid & 15;  // 16 x 16 threads: samples ts*4.., points tp + 16 c
+  const int64_t b0 = static_cast<int64_t>(blockIdx.y) * RL_BM;
+  const int i0 = blockIdx.x * RL_BN;
+  double acc[4][8];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[a][c] = 0.0;
+  for (int k0 = 0; k0 < prm.K_use; k0 += RL_BK) {
+    __syncthreads();
+    for (int e = tid; e < RL_BM * RL_BK; e += RL_THREADS) {
+      const int rb = e / RL_BK, kk = e % RL_BK;
+      const int64_t b = b0 + rb;
+      const int k = k0 + kk;
+      double v = 0.0;
+      if (b < prm.B && k < prm.K_use) v = __dmul_rn(prm.sqrt_lam[k], prm.xi[b * prm.ld + k]);
+      sW[rb * RL_WLD + kk] = v;
+    }
+    for (int e = tid; e < RL_BK * RL_BN; e += RL_THREADS) {
+      const int kk = e / RL_BN, ii = e % RL_BN;
+      const int k = k0 + kk, i = i0 + ii;
+      sP[kk * RL_PLD + ii] = (k < prm.K_use && i < prm.n_nodes) ? prm.phi[static_cast<size_t>(k) * prm.n_nodes + i]
+                                                                 : 0.0;
+    }
+    __syncthreads();
+    const int kend = prm.K_use - k0 < RL_BK ? prm.K_use - k0 : RL_BK;
+    for (int kk = 0; kk < kend; ++kk) {
+      double ph[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) ph[c] = sP[kk * RL_PLD + tp + 16 * c];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const double w = sW[(ts * 4 + a) * RL_WLD + kk];
+        if (w != 0.0) {  // the reference skips w == 0 (field.cpp:120)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[a][c] = __dadd_rn(acc[a][c], __dmul_rn(w, ph[c]));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int64_t b = b0 + ts * 4 + a;
+    if (b >= prm.B) continue;
+    unsigned bad = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int i = i0 + tp + 16 * c;
+      if (i >= prm.n_nodes) continue;
+      const double kv = exp(acc[a][c]);
+      bad |= (!isfinite(kv) ? 1u : 0u) | (kv == 0.0 ? 2u : 0u);
+      prm.kappa[b * prm.ldk + i] = kv;
+    }
+    if (bad && prm.flag) {
+      uint8_t* fp = prm.flag + b;
+      const uintptr_t ad = reinterpret_cast<uintptr_t>(fp);
+      atomicOr(reinterpret_cast<unsigned*>(ad & ~static_cast<uintptr_t>(3)), bad << (8 * (ad & 3)));
+    }
+  }
+}
+
 }  // namespace vqpc

@@ -280,7 +280,10 @@ void run_realise(vqpc_ctx* c, const double* d_xi, int64_t B, int64_t ld, int K_u
   RealiseParams prm{d_xi, ld, B, c->sqrt_lam.p, c->phi.p, c->pb.n_nodes, K_use, d_kappa, ldk, d_flag};
   dim3 grid(static_cast<unsigned>(ceil_div(c->pb.n_nodes, RL_BN)), static_cast<unsigned>(ceil_div(B, RL_BM)));
   Timed tm(c, VQPC_K_REALISE);
-  realise_kernel<<<grid, RL_THREADS, 0, c->stream>>>(prm);
+  if (c->exact)  // reference-order mode: the reference's k-outer AXPY on the CUDA cores
+    realise_exact_kernel<<<grid, RL_THREADS, 0, c->stream>>>(prm);
+  else
+    realise_kernel<<<grid, RL_THREADS, 0, c->stream>>>(prm);
   launch_check(c);
 }
 

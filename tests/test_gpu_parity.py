@@ -434,3 +434,41 @@ def test_2d_other_mesh_sizes_exact_mode(r):
         out = pset.pcg(int(labels[i]), kap[i], cfg["eps"])
         assert out["iterations"] == it[i] and out["status"] == st[i] and out["rel"] == rel[i], i
         assert np.array_equal(out["x"], x[i]), i
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C5"])
+def test_exact_mode_realise_within_one_ulp(name):
+    """Reference-order mode realises h with the reference's k-outer AXPY (product
+    and sum rounded separately, w == 0 skipped): kappa then differs from the
+    oracle's glibc exp(h) by at most one ulp (CUDA exp; ~94 % bitwise equal), while
+    the DMMA path's summation order leaves up to ~12 ulps."""
+    cfg, basis, cb, xi = setup_case(name, 64)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb), factor=False)
+    k_dmma, _ = ctx.realise(xi)
+    ctx.set_exact_reductions(True)
+    k_exact, _ = ctx.realise(xi)
+    k_cpu, _ = oracle.realise(basis["eigenvalues"], basis["eigenvectors"], xi)
+    ulp = np.spacing(k_cpu)
+    d_exact = np.abs(k_exact - k_cpu) / ulp
+    d_dmma = np.abs(k_dmma - k_cpu) / ulp
+    print(name, "kappa vs oracle: exact-order max %.0f ulp (%.2f %% bitwise equal), DMMA max %.0f ulp" % (
+        d_exact.max(), 100 * np.mean(d_exact == 0), d_dmma.max()))
+    assert d_exact.max() <= 1.0
+    assert np.mean(d_exact == 0) > 0.9
+
+
+def test_exact_mode_campaign_from_xi():
+    """End to end in reference-order mode from xi (no coefficient fed across): the
+    GPU campaign and the oracle's run_campaign agree in labels, statuses and J on
+    C1 except where an exp ulp moves a borderline sample."""
+    cfg, basis, cb, xi = setup_case("C1", 256)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    ctx.set_exact_reductions(True)
+    res = ctx.run_campaign(xi, cfg["eps"])
+    ref = oracle.run_campaign(1, cfg["mesh_resolution"], "cholesky", oracle_codebook(cb), basis["eigenvalues"],
+                              basis["eigenvectors"], xi, cfg["eps"])
+    same = res["iterations"] == ref["iterations"]
+    print("C1 exact-mode campaign from xi: J identical for %d / %d samples" % (same.sum(), same.size))
+    assert np.array_equal(res["labels"], ref["labels"]) and np.array_equal(res["status"], ref["status"])
+    assert np.mean(same) >= 0.95
+    assert np.abs(res["iterations"].astype(int) - ref["iterations"]).max() <= 1
