@@ -414,9 +414,10 @@ def test_1d_tiny_meshes(N):
         assert out["iterations"] == it[i] and out["rel"] == rel[i] and np.array_equal(out["x"], x[i]), i
 
 
-@pytest.mark.parametrize("r", [4, 17, 100])
+@pytest.mark.parametrize("r", [4, 17, 100, 257])
 def test_2d_other_mesh_sizes_exact_mode(r):
-    """2-D meshes other than C4's (generic kernel instantiation, odd and tiny m):
+    """2-D meshes other than C4's (generic kernel instantiation, odd and tiny m,
+    and the largest supported mesh, m = 256 interior nodes per row):
     reference-order mode is bit-identical to the oracle fed the same kappa."""
     cfg = campaign.scaled(campaign.CONFIGS["C4"], mesh_resolution=r, n_realizations=12, ns=4000)
     basis = campaign.load_or_build_basis(cfg)
@@ -429,9 +430,10 @@ def test_2d_other_mesh_sizes_exact_mode(r):
     labels = oracle.assign(ocb, xi)
     kap, _ = ctx.realise(xi)
     pset = oracle.PreconditionerSet.from_coefficients(2, r, "ic0", kc)
-    it, rel, st, x = ctx.solve_batch(xi, labels, cfg["eps"], want_x=True)
+    cap = 40 if r > 200 else -1  # bounds the serial oracle at the largest mesh
+    it, rel, st, x = ctx.solve_batch(xi, labels, cfg["eps"], max_iter=cap, want_x=True)
     for i in range(len(xi)):
-        out = pset.pcg(int(labels[i]), kap[i], cfg["eps"])
+        out = pset.pcg(int(labels[i]), kap[i], cfg["eps"], max_iter=cap)
         assert out["iterations"] == it[i] and out["status"] == st[i] and out["rel"] == rel[i], i
         assert np.array_equal(out["x"], x[i]), i
 
