@@ -42,13 +42,15 @@ constexpr int P2_T = 256;            // threads per CTA (one per grid row, r <= 
 constexpr int P2_FAC = 4;            // factor vectors per centroid: D, aW, aS, RN(1/D)
 constexpr int P2_MAXL = 2 * P2_T;    // max levels (2m - 1 <= 511)
 
+// Order in which the reference's SparseBuilder sums a row's six diagonal
+// contributions (fem.cpp:177-211: std::sort by column, then duplicates summed in
+// sorted order), per row pattern W | E << 1 | S << 2 | N << 3 of present
+// neighbours; entry k = index (in triangle order) of the k-th term. The same for
+// every structured mesh; filled once on the host with the same std::sort
+// (diag_orders in vqpc.cu).
+__constant__ unsigned char vqpc_dperm[16][6];
+
 struct Grid2D {
-  // order in which the reference's SparseBuilder sums a row's six diagonal
-  // contributions (fem.cpp:177-211: std::sort by column, then duplicates summed
-  // in sorted order), per row pattern W | E << 1 | S << 2 | N << 3 of present
-  // neighbours; entry k = index (in triangle order) of the k-th term. Filled on
-  // the host with the same std::sort (diag_orders in vqpc.cu).
-  unsigned char dperm[16][6];
   int r;       // mesh resolution
   int m;       // interior nodes per row (r - 1)
   int n;       // m * m
@@ -139,9 +141,9 @@ __device__ inline RowCoef assemble_row(const double* kappa, const Grid2D g, int 
   const double n2 = tri_entry(kappa, side, tx, ty, 0, 2, g.h, nullptr);  // N via T2(X,Y): (a, c)
   // the diagonal in the reference's sorted-duplicate order for this row pattern
   const int pat = (ix > 0 ? 1 : 0) | (ix < g.m - 1 ? 2 : 0) | (iy > 0 ? 4 : 0) | (iy < g.m - 1 ? 8 : 0);
-  double diag = dt[g.dperm[pat][0]];
+  double diag = dt[vqpc_dperm[pat][0]];
 #pragma unroll
-  for (int k = 1; k < 6; ++k) diag = __dadd_rn(diag, dt[g.dperm[pat][k]]);
+  for (int k = 1; k < 6; ++k) diag = __dadd_rn(diag, dt[vqpc_dperm[pat][k]]);
   RowCoef rc;
   rc.d = diag;
   rc.w = ix > 0 ? __dadd_rn(w1, w2) : 0.0;

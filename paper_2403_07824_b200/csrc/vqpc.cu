@@ -728,7 +728,9 @@ int vqpc_ctx_create(const vqpc_problem* pb, vqpc_ctx** out) {
       c->g2.n = c->g2.m * c->g2.m;
       c->g2.L = 2 * c->g2.m - 1;
       c->g2.h = 1.0 / pb->size;
-      diag_orders(c->g2.dperm);
+      unsigned char dp[16][6];
+      diag_orders(dp);
+      CK(cudaMemcpyToSymbol(vqpc_dperm, dp, sizeof(dp)));
     }
     if (pb->dim == 1) {
       const PcgVariant* v = pick_pcg(c->n);
