@@ -32,10 +32,12 @@ struct AssignParams {
   int P, m;
   int32_t* labels;      // B
   double* best;         // B (nullable): the winning distance
+  const int* only_if;   // nullable: run only when *only_if != 0 (fallback after assign_mma_kernel)
 };
 
 template <int M, int SPLIT>
 __global__ void __launch_bounds__(AS_THREADS) assign_kernel(const AssignParams prm) {
+  if (prm.only_if && *prm.only_if == 0) return;
   extern __shared__ double sc[];
   constexpr int SLD = M + 1;  // padded stride
   const int tid = threadIdx.x, lane = tid & 31;
@@ -96,6 +98,7 @@ __global__ void __launch_bounds__(AS_THREADS) assign_kernel(const AssignParams p
 // Generic m (eta staged in local memory), used when no specialisation exists.
 template <int SPLIT>
 __global__ void __launch_bounds__(AS_THREADS) assign_kernel_generic(const AssignParams prm) {
+  if (prm.only_if && *prm.only_if == 0) return;
   extern __shared__ double sc[];
   const int M = prm.m, SLD = M + 1;
   const int tid = threadIdx.x, lane = tid & 31;

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "assign.cuh"
+#include "assign_mma.cuh"
 #include "bucket.cuh"
 #include "common.cuh"
 #include "factor.cuh"
@@ -99,6 +100,8 @@ struct vqpc_ctx {
   DBuf<double> fac2, work2;
   DBuf<int> gmap;
   DBuf<double> bvec2;  // per-node right-hand side when it is not uniform (see pcg2d.cuh)
+  DBuf<double> cnorm;  // |c_p|^2 for the contraction form of the assignment (assign_mma.cuh)
+  DBuf<int> aflag;     // assign_mma candidate-list overflow flag
   bool b2_checked = false, b2_uniform = true;
   int exact = 0;  // reference-order mode: serial dot products (2-D); 1-D: pcg1d_exact_kernel
   DBuf<double2> fac_lu;  // 1-D reference-order mode: P x NP {l_j, u_j}, built on first use
@@ -263,13 +266,40 @@ void run_assign(vqpc_ctx* c, const double* d_xi, int64_t B, int64_t ld, const do
   int split = 1;
   if (B * 1 < target && P >= 32) split = 8;
   else if (B < 2 * target && P >= 16) split = 4;
-  AssignParams prm{d_xi, ld, B, d_root, d_sites, P, m, d_labels, d_best};
+  AssignParams prm{d_xi, ld, B, d_root, d_sites, P, m, d_labels, d_best, nullptr};
   const int64_t threads = B * split;
   const int blocks = static_cast<int>(ceil_div(threads, AS_THREADS));
   AssignFn fn = pick_assign(m, split);
   const size_t smem = AS_TILE_DOUBLES * sizeof(double);
   CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   Timed tm(c, VQPC_K_ASSIGN);
+  // large codebooks (C5: m = 64, P = 4096): the distance table as a DMMA contraction with an
+  // exact re-check of the candidates (assign_mma.cuh); the direct kernel then runs only if a
+  // candidate list overflowed (device-side flag, no host synchronisation)
+  static const bool direct_only = std::getenv("VQPC_ASSIGN_DIRECT") != nullptr;
+  if (!direct_only && d_sites == c->sites.p && (m == 32 || m == 64) && P >= 256) {
+    if (!c->cnorm.p) {
+      c->cnorm.ensure(P);
+      centroid_norms_kernel<<<static_cast<unsigned>(ceil_div(P, 128)), 128, 0, c->stream>>>(d_sites, P, m,
+                                                                                             c->cnorm.p);
+      launch_check(c);
+    }
+    c->aflag.ensure(1);
+    CK(cudaMemsetAsync(c->aflag.p, 0, sizeof(int), c->stream));
+    AssignMmaParams am{d_xi, ld, B, d_root, d_sites, c->cnorm.p, P, d_labels, d_best, c->aflag.p};
+    const unsigned gb = static_cast<unsigned>(ceil_div(B, AM_BM));
+    if (m == 64) {
+      CK(cudaFuncSetAttribute(assign_mma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(assign_mma_smem<64>())));
+      assign_mma_kernel<64><<<gb, AM_THREADS, assign_mma_smem<64>(), c->stream>>>(am);
+    } else {
+      CK(cudaFuncSetAttribute(assign_mma_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(assign_mma_smem<32>())));
+      assign_mma_kernel<32><<<gb, AM_THREADS, assign_mma_smem<32>(), c->stream>>>(am);
+    }
+    launch_check(c);
+    prm.only_if = c->aflag.p;
+  }
   fn<<<blocks, AS_THREADS, smem, c->stream>>>(prm);
   launch_check(c);
 }
@@ -788,6 +818,8 @@ void vqpc_ctx_destroy(vqpc_ctx* c) {
   c->err.release();
   c->gmap.release();
   c->bvec2.release();
+  c->cnorm.release();
+  c->aflag.release();
   for (auto& r : c->recs) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);

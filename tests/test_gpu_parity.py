@@ -474,3 +474,31 @@ def test_exact_mode_campaign_from_xi():
     assert np.array_equal(res["labels"], ref["labels"]) and np.array_equal(res["status"], ref["status"])
     assert np.mean(same) >= 0.95
     assert np.abs(res["iterations"].astype(int) - ref["iterations"]).max() <= 1
+
+
+@pytest.mark.parametrize("m,P", [(64, 4096), (32, 512), (64, 300)])
+def test_assign_contraction_ties_and_near_ties(m, P):
+    """The contraction-plus-recheck assignment (assign_mma.cuh) against the
+    reference's serial nearest_row: duplicated centroids (exact ties: smallest p
+    wins), samples placed exactly on centroids, samples a few ulps apart from a
+    midpoint between two centroids, a non-finite sample."""
+    rs = np.random.default_rng(m + P)
+    lam = np.sort(rs.uniform(1e-3, 0.3, m))[::-1].copy()
+    cen = rs.standard_normal((P, m)) * np.sqrt(lam)
+    cen[P // 2] = cen[3]          # exact duplicate: ties resolve to p = 3
+    cen[P - 1] = cen[P // 3]
+    xi = rs.standard_normal((3000, m))
+    root = np.sqrt(lam)
+    xi[:40] = cen[rs.integers(0, P, 40)] / root            # on a centroid (up to the division)
+    mid = 0.5 * (cen[7] + cen[11]) / root
+    for i in range(40, 60):
+        xi[i] = np.nextafter(mid, mid + (i - 50))             # around the midpoint of 7 and 11
+    xi[60, 5] = np.nan
+    basis = dict(eigenvalues=np.concatenate([lam, lam[-1:] * 0.5]), eigenvectors=rs.standard_normal((m + 1, 50)))
+    cb = dict(method="kmeans", map="scale", lambdas=lam, centroids=cen)
+    ctx = lib.Context(1, 50, basis, cb, "cholesky")
+    lab = ctx.assign(xi)
+    ref = oracle.assign(oracle.Codebook("kmeans", "scale", lam, cen), np.where(np.isfinite(xi), xi, 0.0))
+    ref[60] = -1
+    assert np.array_equal(lab, ref), np.nonzero(lab != ref)[0][:10]
+    assert not (lab == P // 2).any() and not (lab == P - 1).any()  # later duplicates never win
