@@ -101,6 +101,8 @@ struct vqpc_ctx {
   DBuf<int> gmap;
   DBuf<double> bvec2;  // per-node right-hand side when it is not uniform (see pcg2d.cuh)
   DBuf<double> cnorm;  // |c_p|^2 for the contraction form of the assignment (assign_mma.cuh)
+  cudaStream_t aux = nullptr;              // chunks beyond the solve subset (overlap with the PCG)
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   DBuf<int> aflag;     // assign_mma candidate-list overflow flag
   bool b2_checked = false, b2_uniform = true;
   int exact = 0;  // reference-order mode: serial dot products (2-D); 1-D: pcg1d_exact_kernel
@@ -655,7 +657,24 @@ void campaign_device(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, double 
   double* const kappa_scratch = c->kappa.p + static_cast<size_t>(keep) * ldk;  // rows of unsolved chunks
   uint8_t* const kflag_scratch = c->kflag.p + keep;
   if (merge) CK(cudaMemsetAsync(c->kflag.p, 0, keep, c->stream));
-  for (int64_t c0 = 0; c0 < B; c0 += chunk) {
+  // Merged solve with chunks entirely beyond the solve subset (C5: 60 of 64 chunks are
+  // realised and assigned only): those chunks run on a second stream after the merged
+  // PCG launch, so their kernels fill the SMs the PCG's work-queue tail leaves idle
+  // instead of preceding the solve. They touch only the scratch rows and their own
+  // labels/records; the stats kernel waits for them.
+  const bool overlap = merge && nsolve < B && std::getenv("VQPC_NO_OVERLAP") == nullptr;
+  const int64_t split_c0 = overlap ? std::min<int64_t>(B, ceil_div(nsolve, chunk) * chunk) : B;
+  auto realise_assign_only = [&](int64_t c0) {  // a chunk beyond the solve subset
+    const int64_t nb = std::min(chunk, B - c0);
+    const double* xi = d_xi + c0 * ld;
+    run_assign(c, xi, nb, ld, root, c->sites.p, P, c->pb.m, d_labels + c0, nullptr);
+    CK(cudaMemsetAsync(kflag_scratch, 0, nb, c->stream));
+    run_realise(c, xi, nb, ld, c->pb.n_kl, kappa_scratch, ldk, kflag_scratch);
+    mark_unsolved_kernel<<<static_cast<unsigned>(ceil_div(nb, 256)), 256, 0, c->stream>>>(
+        d_iters + c0, d_rel + c0, d_status + c0, nb);
+    launch_check(c);
+  };
+  for (int64_t c0 = 0; c0 < split_c0; c0 += chunk) {
     const int64_t nb = std::min(chunk, B - c0);
     const double* xi = d_xi + c0 * ld;
     run_assign(c, xi, nb, ld, root, c->sites.p, P, c->pb.m, d_labels + c0, nullptr);
@@ -684,10 +703,29 @@ void campaign_device(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, double 
     run_pcg(c, kap, ldk, kfl, c->perm.p, d_labels + c0, nb, c0, eps, max_iter, nullptr, d_iters, d_rel, d_status,
             d_x, solve_limit);
   }
+  if (overlap && split_c0 < B) {
+    if (!c->aux) CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    if (!c->ev_a) CK(cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming));
+    if (!c->ev_b) CK(cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming));
+    CK(cudaEventRecord(c->ev_a, c->stream));  // the solve subset is assigned and realised
+  }
   if (merge) {
     run_schedule(c, d_xi, ld, d_labels, nsolve, root);
     run_pcg(c, c->kappa.p, ldk, c->kflag.p, c->perm.p, d_labels, nsolve, 0, eps, max_iter, nullptr, d_iters,
             d_rel, d_status, d_x, solve_limit);
+  }
+  if (overlap && split_c0 < B) {
+    CK(cudaStreamWaitEvent(c->aux, c->ev_a, 0));
+    std::swap(c->stream, c->aux);  // every launch helper (and its event timing) uses c->stream
+    try {
+      for (int64_t c0 = split_c0; c0 < B; c0 += chunk) realise_assign_only(c0);
+    } catch (...) {
+      std::swap(c->stream, c->aux);
+      throw;
+    }
+    std::swap(c->stream, c->aux);
+    CK(cudaEventRecord(c->ev_b, c->aux));
+    CK(cudaStreamWaitEvent(c->stream, c->ev_b, 0));
   }
   CK(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 4 * P, c->stream));
   CK(cudaMemsetAsync(d_summary, 0, sizeof(int64_t) * 4, c->stream));
@@ -819,6 +857,9 @@ void vqpc_ctx_destroy(vqpc_ctx* c) {
   c->gmap.release();
   c->bvec2.release();
   c->cnorm.release();
+  if (c->aux) cudaStreamDestroy(c->aux);
+  if (c->ev_a) cudaEventDestroy(c->ev_a);
+  if (c->ev_b) cudaEventDestroy(c->ev_b);
   c->aflag.release();
   for (auto& r : c->recs) {
     cudaEventDestroy(r.a);
