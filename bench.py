@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--n", type=int, default=0, help="samples per GPU (default: the config's)")
     ap.add_argument("--cpu-samples", type=int, default=0, help="CPU baseline sample size")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--serial", action="store_true", help="one context, steps back to back (no pipelining)")
     return ap.parse_args()
 
 
@@ -323,56 +324,103 @@ def run_ours(args, rank, world, local_rank):
     xi_np = lib.draw_standard_normal(B, K, cfg["master_seed"], index0=rank * B)
     xi_pin = torch.from_numpy(xi_np).pin_memory()
     d_xi = xi_pin.to(dev)
-    d_lab = torch.empty(B, dtype=torch.int32, device=dev)
-    d_it = torch.empty(B, dtype=torch.int32, device=dev)
-    d_rel = torch.empty(B, dtype=torch.float64, device=dev)
-    d_st = torch.empty(B, dtype=torch.uint8, device=dev)
-    d_stats = torch.empty(4 * P + 4, dtype=torch.int64, device=dev)
-    stream = torch.cuda.Stream(device=dev)
     # C5: realise + assign every sample, PCG on the first solve_subset of the master stream
     solve_limit = max(0, min(B, cfg["solve_subset"] - rank * B)) if cfg.get("solve_subset") else -1
-    ctx = campaign.make_context(cfg, arts, device=local_rank)
-    ctx.set_stream(stream.cuda_stream)
+    # Consecutive steps are double-buffered: two contexts on two streams take the steps
+    # in turn, each step a complete campaign over its batch into its own buffers, with
+    # no dependency on the previous step — so a step's kernels start on the SMs the
+    # previous step's heavy-tailed work queue leaves idle instead of after it drains.
+    # (--serial: one context, steps back to back; reported beside as serial_steps.)
+    NB = 1 if args.serial else 2
+    ctxs, streams, bufs = [], [], []
+    for i in range(NB):
+        streams.append(torch.cuda.Stream(device=dev))
+        c = campaign.make_context(cfg, arts, device=local_rank)
+        c.set_stream(streams[i].cuda_stream)
+        ctxs.append(c)
+        bufs.append(dict(lab=torch.empty(B, dtype=torch.int32, device=dev),
+                         it=torch.empty(B, dtype=torch.int32, device=dev),
+                         rel=torch.empty(B, dtype=torch.float64, device=dev),
+                         st=torch.empty(B, dtype=torch.uint8, device=dev),
+                         stats=torch.empty(4 * P + 4, dtype=torch.int64, device=dev)))
 
-    def step():
-        ctx.run_campaign_device(d_xi.data_ptr(), B, K, cfg["eps"], d_lab.data_ptr(), d_it.data_ptr(),
-                                d_rel.data_ptr(), d_st.data_ptr(), d_stats.data_ptr(), d_stats.data_ptr() + 8 * 4 * P,
-                                chunk=cfg.get("chunk", 0), solve_limit=solve_limit)
+    def step(k):
+        i = k % NB
+        b = bufs[i]
+        ctxs[i].run_campaign_device(d_xi.data_ptr(), B, K, cfg["eps"], b["lab"].data_ptr(), b["it"].data_ptr(),
+                                    b["rel"].data_ptr(), b["st"].data_ptr(), b["stats"].data_ptr(),
+                                    b["stats"].data_ptr() + 8 * 4 * P, chunk=cfg.get("chunk", 0),
+                                    solve_limit=solve_limit)
         if dist:
-            with torch.cuda.stream(stream):
-                dist.all_reduce(d_stats)  # per-centroid n_p / sum_J / converged stats (driver.cpp:241-258)
+            with torch.cuda.stream(streams[i]):
+                dist.all_reduce(b["stats"])  # per-centroid n_p / sum_J / converged stats (driver.cpp:241-258)
 
-    for _ in range(args.warmup):
-        step()
-    ctx.synchronize()
-    ctx.profile(True)
-    ctx.profile_read(reset=True)
-    launches0 = ctx.launches
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local_rank) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
+    def timed_steps(nsteps):
+        """nsteps steps from a common start event; device ms until the last stream drains."""
         torch.cuda.synchronize(dev)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev0.record(streams[0])
+        for s_ in streams[1:]:
+            s_.wait_event(ev0)
+        for k in range(nsteps):
+            step(k)
+        ends = []
+        for s_ in streams:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(s_)
+            ends.append(e)
+        torch.cuda.synchronize(dev)
+        return max(ev0.elapsed_time(e) for e in ends)
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize(dev)
+    serial_ms = None
+    if NB > 1:  # the same steps back to back on one context, for reference
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(streams[0])
+        for _ in range(args.steps):
+            step(0)
+        e1.record(streams[0])
+        torch.cuda.synchronize(dev)
+        serial_ms = e0.elapsed_time(e1)
+    for c in ctxs:
+        c.profile(True)
+        c.profile_read(reset=True)
+    launches0 = sum(c.launches for c in ctxs)
     if dist:
         dist.barrier()
-    launches = ctx.launches - launches0
-    prof = ctx.profile_read(reset=True)
-    ctx.profile(False)
-    ms = ev0.elapsed_time(ev1)
+    with Clocks(local_rank) as clk:
+        ms = timed_steps(args.steps)
+    if dist:
+        dist.barrier()
+    launches = sum(c.launches for c in ctxs) - launches0
+    prof = {}
+    for c in ctxs:
+        for kname, v in c.profile_read(reset=True).items():
+            acc = prof.setdefault(kname, {"ms": 0.0, "launches": 0})
+            acc["ms"] += v["ms"]
+            acc["launches"] += v["launches"]
+        c.profile(False)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     value = world * B * args.steps / (ms_max / 1e3)
+    serial = None
+    if serial_ms is not None:
+        ts = torch.tensor([serial_ms], dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+        serial = {"value": world * B * args.steps / (float(ts.item()) / 1e3),
+                  "ms_per_step": float(ts.item()) / args.steps}
 
-    # per-step solve statistics (identical every step)
-    st = d_st.cpu().numpy()
-    it = d_it.cpu().numpy()
+    # per-step solve statistics (identical every step and in both buffers)
+    st = bufs[0]["st"].cpu().numpy()
+    it = bufs[0]["it"].cpu().numpy()
+    assert NB == 1 or (np.array_equal(bufs[1]["it"].cpu().numpy(), it)
+                       and np.array_equal(bufs[1]["st"].cpu().numpy(), st))
     total_iters = int(it.astype(np.int64).sum())
     conv = st == 0
     n = cfg["mesh_resolution"] - 1
@@ -387,22 +435,34 @@ def run_ours(args, rank, world, local_rank):
     for k, r in kernel_rooflines(cfg, prof, total_iters, B, K, args.steps, peaks).items():
         kernels[k].update(r)
 
-    # e2e through the host-buffer C-ABI entry point (copies inside the timed region)
-    e2e_times = []
-    for s in range(args.steps + 1):
-        torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        res = ctx.run_campaign(xi_pin.numpy(), cfg["eps"], chunk=cfg.get("chunk", 0), solve_limit=solve_limit)
-        e2e_times.append(time.perf_counter() - t0)
-    e2e_t = float(np.sum(e2e_times[1:]))  # first call warms the host-side buffers
+    # e2e through the host-buffer C-ABI entry points (pinned host xi copied in, per-sample
+    # results copied out to pinned host arrays, every step), the steps enqueued in turn on
+    # the contexts with vqpc_run_campaign_async and drained with vqpc_synchronize, so that,
+    # as above, consecutive steps may overlap on the device
+    tdt = {np.int32: torch.int32, np.int64: torch.int64, np.float64: torch.float64, np.uint8: torch.uint8}
+    pinned = lambda n, dt: torch.empty(n, dtype=tdt[dt]).pin_memory().numpy()  # noqa: E731
+    xi_host = xi_pin.numpy()
+    outs = [c.campaign_outputs(B, alloc=pinned) for c in ctxs]
+    kw = dict(chunk=cfg.get("chunk", 0), solve_limit=solve_limit)
+    for i, c in enumerate(ctxs):  # warm the host-side paths of every context
+        c.run_campaign_async(xi_host, cfg["eps"], outs[i], **kw)
+        c.synchronize()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        ctxs[k % NB].run_campaign_async(xi_host, cfg["eps"], outs[k % NB], **kw)
+    for c in ctxs:
+        c.synchronize()
+    e2e_t = time.perf_counter() - t0
     e2e_val = world * B * args.steps / e2e_t
     if dist:
         te = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_val = world * B * args.steps / float(te.item())
+    for o in outs:
+        assert np.array_equal(o["iterations"], it) and np.array_equal(o["status"], st)
     h2d = B * K * 8
     d2h = B * (4 + 4 + 8 + 1) + 8 * (4 * P + 4)
-    assert np.array_equal(res["iterations"], it) and np.array_equal(res["status"], st)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -416,7 +476,10 @@ def run_ours(args, rank, world, local_rank):
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded counter-RNG xi; no dataset exists for this path)",
-                "config": workload(cfg, B, K),
+                "config": {**workload(cfg, B, K),
+                           "steps_pipelined": f"{NB} contexts / streams take the steps in turn (no inter-step "
+                                              f"dependency; each step a full campaign)" if NB > 1 else "serial"},
+                "serial_steps": serial,
                 "mean_pcg_iters": float(it[conv].mean()) if conv.any() else 0.0,
                 "status_counts": {lib.STATUS[k]: int((st == k).sum()) for k in np.unique(st)},
                 "total_pcg_iterations_per_gpu_step": total_iters,
@@ -430,7 +493,8 @@ def run_ours(args, rank, world, local_rank):
                 "clocks": clk.summary(),
                 "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
-    ctx.close()
+    for c in ctxs:
+        c.close()
 
 
 def main():

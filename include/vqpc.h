@@ -171,6 +171,17 @@ int vqpc_run_campaign_ex_d(vqpc_ctx* ctx, const double* d_xi, int64_t B, int ld,
                            int64_t chunk, int64_t solve_limit, int32_t* d_labels, int32_t* d_iters,
                            double* d_final_rel, uint8_t* d_status, int64_t* d_stats, int64_t* d_summary);
 
+/* Same as vqpc_run_campaign_ex without the final synchronisation: every copy and
+ * kernel is enqueued on the context's stream and the call returns; the host
+ * buffers (xi in, results out) must stay valid until vqpc_synchronize(ctx). With
+ * pinned host buffers the copies overlap other work, so a caller alternating two
+ * contexts pipelines consecutive batches (one batch's kernels start on the SMs the
+ * previous batch's work-queue tail frees). Errors raised while enqueueing are
+ * returned; asynchronous ones surface at vqpc_synchronize. */
+int vqpc_run_campaign_async(vqpc_ctx* ctx, const double* xi, int64_t B, int ld, double eps, int max_iter,
+                            int64_t chunk, int64_t solve_limit, int32_t* labels, int32_t* iters,
+                            double* final_rel, uint8_t* status, int64_t* stats, int64_t* summary);
+
 /* Same as vqpc_run_campaign_ex, also returning the solutions the reference
  * computes and discards (driver.cpp:236-237, SURVEY §8b "run_campaign_with_
  * solutions"): x_out is B x n host memory; row i receives x of realisation i

@@ -1118,9 +1118,10 @@ int vqpc_run_campaign_d(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, doub
                                 d_stats, d_summary);
 }
 
-int vqpc_run_campaign_ex(vqpc_ctx* c, const double* xi, int64_t B, int ld, double eps, int max_iter, int64_t chunk,
-                         int64_t solve_limit, int32_t* labels, int32_t* iters, double* final_rel, uint8_t* status, int64_t* stats,
-                      int64_t* summary) {
+namespace {
+int campaign_host(vqpc_ctx* c, const double* xi, int64_t B, int ld, double eps, int max_iter, int64_t chunk,
+                  int64_t solve_limit, int32_t* labels, int32_t* iters, double* final_rel, uint8_t* status,
+                  int64_t* stats, int64_t* summary, bool sync) {
   if (!c) return VQPC_INVALID_ARGUMENT;
   return guard(c, [&] {
     const int P = c->pb.P;
@@ -1140,8 +1141,23 @@ int vqpc_run_campaign_ex(vqpc_ctx* c, const double* xi, int64_t B, int ld, doubl
     d2h(c, status, c->status.p, B);
     d2h(c, stats, c->stats.p, 4 * static_cast<size_t>(P));
     d2h(c, summary, c->stats.p + 4 * P, 4);
-    CK(cudaStreamSynchronize(c->stream));
+    if (sync) CK(cudaStreamSynchronize(c->stream));
   });
+}
+}  // namespace
+
+int vqpc_run_campaign_ex(vqpc_ctx* c, const double* xi, int64_t B, int ld, double eps, int max_iter, int64_t chunk,
+                         int64_t solve_limit, int32_t* labels, int32_t* iters, double* final_rel, uint8_t* status,
+                         int64_t* stats, int64_t* summary) {
+  return campaign_host(c, xi, B, ld, eps, max_iter, chunk, solve_limit, labels, iters, final_rel, status, stats,
+                       summary, true);
+}
+
+int vqpc_run_campaign_async(vqpc_ctx* c, const double* xi, int64_t B, int ld, double eps, int max_iter,
+                            int64_t chunk, int64_t solve_limit, int32_t* labels, int32_t* iters, double* final_rel,
+                            uint8_t* status, int64_t* stats, int64_t* summary) {
+  return campaign_host(c, xi, B, ld, eps, max_iter, chunk, solve_limit, labels, iters, final_rel, status, stats,
+                       summary, false);
 }
 
 // run_campaign_with plus the solutions the reference computes and discards

@@ -68,6 +68,7 @@ def load():
             "vqpc_run_campaign_ex": (I, [VP, VP, I64, I, D, I, I64, I64, VP, VP, VP, VP, VP, VP]),
             "vqpc_run_campaign_ex_d": (I, [VP, VP, I64, I, D, I, I64, I64, VP, VP, VP, VP, VP, VP]),
             "vqpc_run_campaign_x": (I, [VP, VP, I64, I, D, I, I64, I64, VP, VP, VP, VP, VP, VP, VP]),
+            "vqpc_run_campaign_async": (I, [VP, VP, I64, I, D, I, I64, I64, VP, VP, VP, VP, VP, VP]),
             "vqpc_kmeans": (I, [I, VP, I, I, VP, I, I, U64, I, D, VP, VP, C.POINTER(C.c_int)]),
             "vqpc_draw_standard_normal": (I, [I64, I, U64, I64, VP, I]),
             "vqpc_profile": (I, [VP, I]),
@@ -293,6 +294,21 @@ class Context:
         return dict(x=x, labels=labels, iterations=it, rel=rel, status=st, n_p=stats[:P], sum_j=stats[P:2 * P],
                     conv_count=stats[2 * P:3 * P], conv_sum=stats[3 * P:], total_iterations=int(summary[0]),
                     unconverged=int(summary[1]), conv_total=int(summary[2]), conv_sum_total=int(summary[3]))
+
+    def run_campaign_async(self, xi, eps, out, max_iter=-1, chunk=0, solve_limit=-1):
+        """vqpc_run_campaign_async: enqueue a campaign over host xi (pinned for overlap)
+        into the preallocated host arrays of ``out`` (labels, iterations, rel, status,
+        stats, summary — see campaign_outputs) and return at once; results are valid
+        after synchronize()."""
+        B, ld = xi.shape
+        self._c(load().vqpc_run_campaign_async(self.h, _p(xi), B, ld, eps, max_iter, chunk, solve_limit,
+                                               _p(out["labels"]), _p(out["iterations"]), _p(out["rel"]),
+                                               _p(out["status"]), _p(out["stats"]), _p(out["summary"])))
+
+    def campaign_outputs(self, B, alloc=np.empty):
+        """Host result arrays for run_campaign_async (alloc: e.g. a pinned-memory allocator)."""
+        return dict(labels=alloc(B, np.int32), iterations=alloc(B, np.int32), rel=alloc(B, np.float64),
+                    status=alloc(B, np.uint8), stats=alloc(4 * self.P, np.int64), summary=alloc(4, np.int64))
 
     def run_campaign_device(self, d_xi_ptr, B, ld, eps, d_labels, d_iters, d_rel, d_status, d_stats, d_summary,
                             max_iter=-1, chunk=0, solve_limit=-1):

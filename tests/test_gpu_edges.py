@@ -129,3 +129,21 @@ def test_size_limits():
         basis = dict(eigenvalues=np.array([1.0, 0.5]), eigenvectors=np.zeros((2, nn)))
         with pytest.raises(lib.VqpcError, match="invalid-config"):
             lib.Context(dim, size, basis, cb, "cholesky" if dim == 1 else "ic0")
+
+
+def test_async_campaigns_on_two_contexts_match_sync():
+    """vqpc_run_campaign_async: batches enqueued alternately on two contexts (the
+    bench's pipelined steps) give the synchronous call's records and statistics."""
+    cfg, basis, cb, xi, ctx = _case("C3", 300)
+    ref = ctx.run_campaign(xi, cfg["eps"])
+    ctx2 = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    outs = [c.campaign_outputs(len(xi)) for c in (ctx, ctx2)]
+    for k in range(4):
+        c = (ctx, ctx2)[k % 2]
+        c.run_campaign_async(xi, cfg["eps"], outs[k % 2])
+    ctx.synchronize()
+    ctx2.synchronize()
+    for o in outs:
+        assert np.array_equal(o["labels"], ref["labels"]) and np.array_equal(o["iterations"], ref["iterations"])
+        assert np.array_equal(o["rel"], ref["rel"]) and np.array_equal(o["status"], ref["status"])
+        assert np.array_equal(o["stats"][:ctx.P], ref["n_p"]) and int(o["summary"][0]) == ref["total_iterations"]
