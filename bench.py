@@ -344,6 +344,8 @@ def run_ours(args, rank, world, local_rank):
                          st=torch.empty(B, dtype=torch.uint8, device=dev),
                          stats=torch.empty(4 * P + 4, dtype=torch.int64, device=dev)))
 
+    coll = {"last": None}  # event after the previous step's all-reduce
+
     def step(k):
         i = k % NB
         b = bufs[i]
@@ -352,8 +354,16 @@ def run_ours(args, rank, world, local_rank):
                                     b["stats"].data_ptr() + 8 * 4 * P, chunk=cfg.get("chunk", 0),
                                     solve_limit=solve_limit)
         if dist:
+            # collectives of one communicator must run in issue order on every rank: the
+            # all-reduce of step k waits for that of step k-1 (only the reductions are
+            # chained; the steps' kernels stay independent)
+            if coll["last"] is not None:
+                streams[i].wait_event(coll["last"])
             with torch.cuda.stream(streams[i]):
                 dist.all_reduce(b["stats"])  # per-centroid n_p / sum_J / converged stats (driver.cpp:241-258)
+            ev = torch.cuda.Event()
+            ev.record(streams[i])
+            coll["last"] = ev
 
     def timed_steps(nsteps):
         """nsteps steps from a common start event; device ms until the last stream drains."""
