@@ -502,3 +502,40 @@ def test_assign_contraction_ties_and_near_ties(m, P):
     ref[60] = -1
     assert np.array_equal(lab, ref), np.nonzero(lab != ref)[0][:10]
     assert not (lab == P // 2).any() and not (lab == P - 1).any()  # later duplicates never win
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C5"])
+def test_full_size_campaign_invariants(name):
+    """BASELINE sizes (C2: 2^17, C3: 2^16, C5: 2^20 realised/assigned with 2^16
+    solved) through size-independent properties: labels in range and equal to the
+    oracle's on a strided sample; converged records have rel < eps, the others
+    rel >= eps or a breakdown/iteration-cap status; per-centroid statistics equal
+    the per-sample records; J <= 10 n; a second run reproduces every record."""
+    cfg = campaign.CONFIGS[name]
+    arts = campaign.prepare_campaign(cfg)
+    basis, cb = arts["basis"], arts["codebook"]
+    K = basis["eigenvalues"].size
+    B = cfg["n_realizations"]
+    xi = lib.draw_standard_normal(B, K, cfg["master_seed"])
+    ctx = campaign.make_context(cfg, arts)
+    kw = dict(chunk=cfg.get("chunk", 0), solve_limit=cfg.get("solve_subset") or -1)
+    res = ctx.run_campaign(xi, cfg["eps"], **kw)
+    lab, it, st, rel = res["labels"], res["iterations"], res["status"], res["rel"]
+    P, n = cb["P"], (cfg["mesh_resolution"] - 1) ** cfg["dim"]
+    assert ((lab >= 0) & (lab < P)).all()
+    idx = np.arange(0, B, max(1, B // 2048))
+    assert np.array_equal(lab[idx], oracle.assign(oracle_codebook(cb), xi[idx]))
+    solved = st != 6
+    assert solved.sum() == (cfg.get("solve_subset") or B)
+    conv = st == 0
+    assert (rel[conv] < cfg["eps"]).all()
+    assert (rel[st == 1] >= cfg["eps"]).all() and (it[st == 1] == 10 * n).all()
+    assert (it <= 10 * n).all() and set(np.unique(st)) <= {0, 1, 2, 6}
+    n_p = np.bincount(lab[solved], minlength=P)
+    assert np.array_equal(res["n_p"], n_p)
+    assert np.array_equal(res["sum_j"], np.bincount(lab[solved], weights=it[solved], minlength=P).astype(np.int64))
+    assert np.array_equal(res["conv_count"], np.bincount(lab[conv], minlength=P))
+    assert res["total_iterations"] == int(it[solved].sum()) and res["conv_total"] == int(conv.sum())
+    again = ctx.run_campaign(xi, cfg["eps"], **kw)
+    for k in ("labels", "iterations", "rel", "status", "n_p", "sum_j"):
+        assert np.array_equal(res[k], again[k]), k
