@@ -1,0 +1,605 @@
+// pcgchol2d.cuh — 2-D campaigns with the reference's own `cholesky` preconditioner
+// (proj/src/solver.cpp:72-111, kind "cholesky", driver.hpp:13): every centroid
+// matrix is reordered by reverse Cuthill-McKee (solver.cpp:32-70, computed once
+// on the host: the pattern is the same for every centroid), factored as LL^T over
+// its envelope, and each sample's PCG applies z = P^T L^-T L^-1 P r.
+//
+// (e) cholfactor2d_kernel — one CTA per centroid, the factor BIT-IDENTICAL to the
+//     oracle's restatement of SimplicialLLT's up-looking rows (oracle/src/
+//     vqp_oracle.cpp CholeskyPreconditioner): row k of the permuted matrix is
+//     L_kl = (B_kl - sum_j L_kj L_lj) / L_ll (j ascending, rounded products, no
+//     contraction), L_kk = sqrt(B_kk - sum_l L_kl^2). Rows are dealt round-robin to
+//     the 256 threads; a thread computing L_kl waits on a shared-memory flag until
+//     row l is final, so up to 256 rows advance as a pipelined wavefront.
+//     cholinv_kernel then inverts the 32 x 32 diagonal blocks of L (per centroid,
+//     once) so the in-block part of each triangular solve is a small GEMV.
+// (d) pcgchol2d_kernel<S> — one CTA per group of S samples that share a label
+//     (multi right-hand side: every byte of the factor streamed from HBM serves S
+//     solves). All vectors live in HBM in the RCM order, so the preconditioner's
+//     permutation is free and the stencil product gathers through a neighbour
+//     table. The triangular solves walk the envelope in blocks of 32 rows: a
+//     block's rows are contiguous in L, so one cp.async.bulk (TMA) copy per block
+//     lands them in shared memory, double-buffered on transaction mbarriers.
+//       forward  y_B = Linv_B (r_B - L_{B,<B} y)       (left-looking, warp per row)
+//       backward z_B = Linv_B^T w_B; w_j -= L_{B,j}^T z_B  (right-looking, thread per column)
+//     with y / w in a shared-memory ring of the last PC_RING rows (>= W + 32, W the
+//     envelope width). Dot products are block-tree sums (the throughput mode of
+//     pcg2d); the control flow and the update arithmetic follow solver.cpp:186-245.
+#pragma once
+#include "pcg2d.cuh"
+
+namespace vqpc {
+
+constexpr int PC_T = 256;     // threads per CTA
+constexpr int PC_BS = 32;     // rows per block of the triangular solves
+constexpr int PC_RING = 1024; // y / w ring (rows)
+constexpr int PC_NV = 11;     // per sample slot: D, cS, cW, cE, cN, b, x, r, p, Ap, z
+constexpr int PC_MAXS = 4;
+
+struct CholLayout {
+  int n;                 // unknowns
+  int W;                 // envelope width max_k (k - first[k])
+  int nblk;              // ceil(n / PC_BS)
+  const int* cperm;      // permuted row -> natural interior id (iy * m + ix)
+  const int* first;      // envelope start of each permuted row
+  const int64_t* start;  // offset of row k (entries first[k] .. k) in L; n + 1 entries
+  const int4* nbr;       // permuted rows of the S, W, E, N neighbours (-1: none)
+};
+
+// ---- (e) factor -----------------------------------------------------------------
+__global__ void __launch_bounds__(PC_T) cholfactor2d_kernel(const double* kappa_c, int64_t ldk, int P,
+                                                            const Grid2D g, const CholLayout lay, double* L,
+                                                            int64_t ldL, int* err) {
+  __shared__ int done[PC_T];  // 1 + the last row finished by thread t (its rows ascend)
+  const int p = blockIdx.x, t = threadIdx.x;
+  if (p >= P) return;
+  const double* kap = kappa_c + static_cast<size_t>(p) * ldk;
+  double* Lp = L + static_cast<size_t>(p) * ldL;
+  done[t] = 0;
+  __syncthreads();
+  volatile int* vdone = done;
+  bool ok = true;
+  for (int k = t; k < lay.n; k += PC_T) {
+    const int f = lay.first[k];
+    double* Lk = Lp + lay.start[k] - f;  // Lk[l] = L(k, l)
+    for (int l = f; l <= k; ++l) Lk[l] = 0.0;
+    const int id = lay.cperm[k];
+    const RowCoef rc = assemble_row(kap, g, id % g.m, id / g.m);
+    const int4 nb = lay.nbr[k];
+    if (nb.x >= 0 && nb.x < k) Lk[nb.x] = rc.s;
+    if (nb.y >= 0 && nb.y < k) Lk[nb.y] = rc.w;
+    if (nb.z >= 0 && nb.z < k) Lk[nb.z] = rc.e;
+    if (nb.w >= 0 && nb.w < k) Lk[nb.w] = rc.nn;
+    double d = rc.d;
+    for (int l = f; l < k; ++l) {
+      const int owner = l % PC_T;
+      while (vdone[owner] <= l) {
+      }
+      __threadfence_block();
+      const int fl = lay.first[l];
+      const double* Ll = Lp + lay.start[l] - fl;
+      double s = Lk[l];
+      for (int j = f > fl ? f : fl; j < l; ++j) s = __dsub_rn(s, __dmul_rn(Lk[j], Ll[j]));
+      const double lkl = __ddiv_rn(s, Ll[l]);
+      Lk[l] = lkl;
+      d = __dsub_rn(d, __dmul_rn(lkl, lkl));
+    }
+    if (!(d > 0.0)) ok = false;
+    Lk[k] = __dsqrt_rn(d);
+    __threadfence_block();
+    vdone[t] = k + 1;
+  }
+  if (!ok) atomicExch(err, 1);
+}
+
+// inverse of every 32 x 32 diagonal block of L (row-major [i][c], zero above the
+// diagonal; rows past n are identity rows). One thread per (centroid, block, column).
+__global__ void cholinv_kernel(const double* L, int64_t ldL, const CholLayout lay, int P, double* Linv,
+                               int64_t ldLi) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int c = static_cast<int>(idx & 31);
+  const int64_t bp = idx >> 5;
+  if (bp >= static_cast<int64_t>(P) * lay.nblk) return;
+  const int p = static_cast<int>(bp / lay.nblk), blk = static_cast<int>(bp % lay.nblk);
+  const int r0 = blk * PC_BS;
+  const double* Lp = L + static_cast<size_t>(p) * ldL;
+  double* out = Linv + static_cast<size_t>(p) * ldLi + static_cast<size_t>(blk) * PC_BS * PC_BS;
+  double x[PC_BS];
+  for (int i = 0; i < PC_BS; ++i) {
+    const int k = r0 + i;
+    if (k >= lay.n) {
+      x[i] = i == c ? 1.0 : 0.0;
+    } else if (i < c) {
+      x[i] = 0.0;
+    } else {
+      const int f = lay.first[k];
+      const double* Lk = Lp + lay.start[k] - f;
+      double s = i == c ? 1.0 : 0.0;
+      for (int q = (f - r0 > c ? f - r0 : c); q < i; ++q) s = fma(-Lk[r0 + q], x[q], s);
+      x[i] = s / Lk[k];
+    }
+  }
+  for (int i = 0; i < PC_BS; ++i) out[i * PC_BS + c] = x[i];
+}
+
+// Work groups: up to S consecutive entries of a label bucket (perm is label-major,
+// predicted-cost-descending inside a bucket). Emitted q-major — the q-th group of
+// every label before any (q+1)-th — so every factor's heaviest samples go first.
+__global__ void chol_groups_kernel(const int64_t* offsets, int P, int S, int2* groups, int* ngroups) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int ng = 0;
+  for (int64_t q = 0;; ++q) {
+    bool any = false;
+    for (int p = 0; p <= P; ++p) {
+      const int64_t lo = offsets[p] + q * S, hi = offsets[p + 1];
+      if (lo < hi) {
+        groups[ng++] = make_int2(static_cast<int>(lo), static_cast<int>(hi - lo < S ? hi - lo : S));
+        any = true;
+      }
+    }
+    if (!any) break;
+  }
+  *ngroups = ng;
+}
+
+struct PcholParams {
+  Grid2D g;
+  CholLayout lay;
+  const double* kappa;  // samples x ldk nodal kappa
+  int64_t ldk;
+  const uint8_t* kflag;
+  const int32_t* perm;  // label-major order
+  const int32_t* labels;
+  const int2* groups;
+  const int* ngroups;
+  const double* L;      // P x ldL envelope factors
+  int64_t ldL;
+  const double* Linv;   // P x ldLi inverted diagonal blocks
+  int64_t ldLi;
+  int cap;              // doubles per staged block (max over blocks, 16-byte padded)
+  double* work;         // per CTA: S * PC_NV * n doubles
+  int64_t B, out_base, solve_limit;
+  double eps;
+  int max_iter;
+  const int32_t* max_iter_arr;
+  int* counter;
+  int32_t* iters;
+  double* rel;
+  uint8_t* status;
+  double* x_out;        // nullable, natural interior order
+};
+
+__device__ __forceinline__ void pc_bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void pc_mbar_init(unsigned bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void pc_mbar_expect(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void pc_mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n PC_WAIT:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra PC_WAIT;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+template <int S>
+__device__ __forceinline__ void pc_block_sums(double (&v)[S], double (*red)[PC_T / 32], int warp, int lane) {
+#pragma unroll
+  for (int s = 0; s < S; ++s) v[s] = warp_allsum(v[s]);
+  if (lane == 0)
+#pragma unroll
+    for (int s = 0; s < S; ++s) red[s][warp] = v[s];
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    double a[PC_T / 32];
+#pragma unroll
+    for (int i = 0; i < PC_T / 32; ++i) a[i] = red[s][i];
+#pragma unroll
+    for (int w = 1; w < PC_T / 32; w <<= 1)
+#pragma unroll
+      for (int i = 0; i + w < PC_T / 32; i += 2 * w) a[i] += a[i + w];
+    v[s] = a[0];
+  }
+  __syncthreads();
+}
+
+template <int S>
+__global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams prm) {
+  extern __shared__ __align__(128) double dsm[];
+  __shared__ __align__(8) unsigned long long mbar[2];
+  __shared__ double red[S][PC_T / 32];
+  __shared__ double tv[S][PC_BS];
+  __shared__ int s_first[PC_BS];
+  __shared__ int64_t s_start[PC_BS];
+  __shared__ int s_grp;
+  const Grid2D g = prm.g;
+  const CholLayout lay = prm.lay;
+  const int n = lay.n, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int stage_len = prm.cap + PC_BS * PC_BS;
+  double* ring = dsm + 2 * stage_len;  // [S][PC_RING]
+  const unsigned bar0 = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[0]));
+  if (t == 0) {
+    pc_mbar_init(bar0);
+    pc_mbar_init(bar0 + 8);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double* base = prm.work + static_cast<size_t>(blockIdx.x) * S * PC_NV * n;
+  auto vec = [&](int s, int v) { return base + (static_cast<size_t>(s) * PC_NV + v) * n; };
+  enum { VD = 0, VS, VW, VE, VN, VB, VX, VR, VP, VAP, VZ };
+  int64_t vg = 0;  // staged-block visits issued by this CTA (mbarrier phases)
+  const int nvis = 2 * lay.nblk;
+
+  for (;;) {
+    if (t == 0) s_grp = atomicAdd(prm.counter, 1);
+    __syncthreads();
+    const int grp = s_grp;
+    __syncthreads();
+    if (grp >= *prm.ngroups) break;
+    const int2 gr = prm.groups[grp];
+    int sid[S];
+    int64_t gsv[S];
+    bool act[S];
+    int J[S], mit[S];
+    double rel_rec[S], norm_b[S], rz[S], beta[S], alpha[S];
+    uint8_t st[S];
+    int label = 0;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      act[s] = false;
+      J[s] = 0;
+      rel_rec[s] = 0.0;
+      st[s] = VQPC_S_MAX_ITER;
+      sid[s] = -1;
+      gsv[s] = 0;
+      if (s < gr.y) {
+        const int sm = prm.perm[gr.x + s];
+        sid[s] = sm;
+        gsv[s] = prm.out_base + sm;
+        const int lb = prm.labels[sm];
+        if (lb < 0 || prm.kflag[sm] || gsv[s] >= prm.solve_limit) {
+          st[s] = gsv[s] >= prm.solve_limit ? VQPC_S_NOT_SOLVED
+                  : lb < 0                  ? VQPC_S_INVALID_LATENT
+                                            : (prm.kflag[sm] & 1) ? VQPC_S_COEFF_OVERFLOW : VQPC_S_INVALID_COEFF;
+        } else {
+          act[s] = true;
+          label = lb;  // a group shares one label (bucketed)
+        }
+        mit[s] = prm.max_iter_arr ? prm.max_iter_arr[gsv[s]] : (prm.max_iter < 0 ? 10 * n : prm.max_iter);
+      }
+    }
+    const double* Lp = prm.L + static_cast<size_t>(label) * prm.ldL;
+    const double* Lip = prm.Linv + static_cast<size_t>(label) * prm.ldLi;
+
+    // ---- setup: rows of every sample in RCM order; x = 0, r = b ---------------------
+    double part[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      part[s] = 0.0;
+      if (!act[s]) continue;
+      const double* kap = prm.kappa + static_cast<size_t>(sid[s]) * prm.ldk;
+      for (int k = t; k < n; k += PC_T) {
+        const int id = lay.cperm[k];
+        const RowCoef rc = assemble_row(kap, g, id % g.m, id / g.m);
+        vec(s, VD)[k] = rc.d;
+        vec(s, VS)[k] = rc.s;
+        vec(s, VW)[k] = rc.w;
+        vec(s, VE)[k] = rc.e;
+        vec(s, VN)[k] = rc.nn;
+        vec(s, VB)[k] = rc.b;
+        vec(s, VX)[k] = 0.0;
+        vec(s, VR)[k] = rc.b;
+        part[s] = fma(rc.b, rc.b, part[s]);
+      }
+    }
+    pc_block_sums<S>(part, red, warp, lane);
+#pragma unroll
+    for (int s = 0; s < S; ++s) norm_b[s] = sqrt(part[s]);
+
+    // ---- z = M^{-1} r for every slot of the group; returns the r.z partials --------
+    auto issue = [&](int v) {
+      if (t != 0 || v >= nvis) return;
+      const int blk = v < lay.nblk ? v : nvis - 1 - v;
+      const int r0 = blk * PC_BS, r1 = min(n, r0 + PC_BS);
+      const int64_t a0 = lay.start[r0] & ~1ll, a1 = (lay.start[r1] + 1) & ~1ll;
+      const int64_t gv = vg + v;
+      const int stg = static_cast<int>(gv & 1);
+      double* sp = dsm + stg * stage_len;
+      const unsigned bar = bar0 + 8u * stg;
+      const unsigned cbytes = static_cast<unsigned>((a1 - a0) * 8);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      pc_mbar_expect(bar, cbytes + PC_BS * PC_BS * 8u);
+      pc_bulk_g2s(static_cast<unsigned>(__cvta_generic_to_shared(sp)),
+                  Lip + static_cast<size_t>(blk) * PC_BS * PC_BS, PC_BS * PC_BS * 8u, bar);
+      pc_bulk_g2s(static_cast<unsigned>(__cvta_generic_to_shared(sp + PC_BS * PC_BS)), Lp + a0, cbytes, bar);
+    };
+    auto solve = [&](double (&rzp)[S]) {
+#pragma unroll
+      for (int s = 0; s < S; ++s) rzp[s] = 0.0;
+      __syncthreads();
+      issue(0);
+      issue(1);
+      int init_lo = n;
+      for (int v = 0; v < nvis; ++v) {
+        const bool fwd = v < lay.nblk;
+        const int blk = fwd ? v : nvis - 1 - v;
+        const int r0 = blk * PC_BS, r1 = min(n, r0 + PC_BS);
+        const int64_t gv = vg + v;
+        const int stg = static_cast<int>(gv & 1);
+        const double* Li = dsm + stg * stage_len;
+        const double* ch = Li + PC_BS * PC_BS - (lay.start[r0] & ~1ll);  // ch[start-index] = L value
+        if (t < PC_BS) {
+          const int k = r0 + t;
+          s_first[t] = k < n ? lay.first[k] : k;
+          s_start[t] = k < n ? lay.start[k] : 0;
+        }
+        if (fwd) {
+          double rk[S][4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int k = r0 + 4 * warp + i;
+#pragma unroll
+            for (int s = 0; s < S; ++s) rk[s][i] = (lane == 0 && k < r1) ? vec(s, VR)[k] : 0.0;
+          }
+          __syncthreads();
+          pc_mbar_wait(bar0 + 8u * stg, static_cast<unsigned>((gv >> 1) & 1));
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int ii = 4 * warp + i, k = r0 + ii;
+            double acc[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) acc[s] = 0.0;
+            if (k < r1) {
+              const int f = s_first[ii];
+              const double* row = ch + (s_start[ii] - f);
+              for (int j = f + lane; j < r0; j += 32) {
+                const double lv = row[j];
+#pragma unroll
+                for (int s = 0; s < S; ++s) acc[s] = fma(lv, ring[s * PC_RING + (j & (PC_RING - 1))], acc[s]);
+              }
+            }
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+              acc[s] = warp_allsum(acc[s]);
+              if (lane == 0) tv[s][ii] = k < r1 ? rk[s][i] - acc[s] : 0.0;
+            }
+          }
+          __syncthreads();
+          const int i = t >> 3, q = t & 7;
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            double y = 0.0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) y = fma(Li[i * PC_BS + 4 * q + c], tv[s][4 * q + c], y);
+            y += shfl_xor(y, 1);
+            y += shfl_xor(y, 2);
+            y += shfl_xor(y, 4);
+            if (q == 0 && r0 + i < r1) {
+              ring[s * PC_RING + ((r0 + i) & (PC_RING - 1))] = y;
+              vec(s, VZ)[r0 + i] = y;
+            }
+          }
+          __syncthreads();
+        } else {
+          // w ring: rows entering the window take their y
+          const int new_lo = r0 - lay.W > 0 ? r0 - lay.W : 0;
+          for (int j = new_lo + t; j < init_lo; j += PC_T)
+#pragma unroll
+            for (int s = 0; s < S; ++s) ring[s * PC_RING + (j & (PC_RING - 1))] = vec(s, VZ)[j];
+          init_lo = new_lo < init_lo ? new_lo : init_lo;
+          __syncthreads();
+          pc_mbar_wait(bar0 + 8u * stg, static_cast<unsigned>((gv >> 1) & 1));
+          const int c = t >> 3, q = t & 7;
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            double z = 0.0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int i = 4 * q + e;
+              const double w = r0 + i < r1 ? ring[s * PC_RING + ((r0 + i) & (PC_RING - 1))] : 0.0;
+              z = fma(Li[i * PC_BS + c], w, z);
+            }
+            z += shfl_xor(z, 1);
+            z += shfl_xor(z, 2);
+            z += shfl_xor(z, 4);
+            if (q == 0) {
+              tv[s][c] = r0 + c < r1 ? z : 0.0;
+              if (r0 + c < r1) {
+                vec(s, VZ)[r0 + c] = z;
+                rzp[s] = fma(vec(s, VR)[r0 + c], z, rzp[s]);
+              }
+            }
+          }
+          __syncthreads();
+          for (int j = new_lo + t; j < r0; j += PC_T) {
+            double acc[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) acc[s] = 0.0;
+#pragma unroll 4
+            for (int i = 0; i < r1 - r0; ++i) {
+              const int f = s_first[i];
+              if (j >= f) {
+                const double lv = ch[s_start[i] - f + j];
+#pragma unroll
+                for (int s = 0; s < S; ++s) acc[s] = fma(lv, tv[s][i], acc[s]);
+              }
+            }
+#pragma unroll
+            for (int s = 0; s < S; ++s) ring[s * PC_RING + (j & (PC_RING - 1))] -= acc[s];
+          }
+          __syncthreads();
+        }
+        issue(v + 2);
+      }
+      vg += nvis;
+      pc_block_sums<S>(rzp, red, warp, lane);
+    };
+
+    bool any0 = false;
+#pragma unroll
+    for (int s = 0; s < S; ++s) any0 |= act[s];
+    double rzp[S];
+    if (any0) solve(rzp);
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      rz[s] = rzp[s];
+      beta[s] = 0.0;
+      if (!act[s]) continue;
+      if (norm_b[s] == 0.0) {
+        st[s] = VQPC_S_CONVERGED;
+        act[s] = false;
+      } else if (!(rz[s] > 0.0)) {
+        st[s] = VQPC_S_BREAKDOWN;
+        act[s] = false;
+      } else if (mit[s] < 1) {
+        act[s] = false;
+      }
+    }
+    for (int j = 1;; ++j) {
+      bool any = false;
+#pragma unroll
+      for (int s = 0; s < S; ++s) any |= act[s];
+      if (!any) break;
+      // p = z + beta p (p = z on the first iteration), solver.cpp:241
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        if (!act[s]) continue;
+        double* P = vec(s, VP);
+        const double* Z = vec(s, VZ);
+        for (int k = t; k < n; k += PC_T) P[k] = j == 1 ? Z[k] : __dadd_rn(Z[k], __dmul_rn(beta[s], P[k]));
+      }
+      __syncthreads();
+      // Ap and p.Ap (CSR column order S, W, diag, E, N; no contraction)
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        part[s] = 0.0;
+        if (!act[s]) continue;
+        const double* P = vec(s, VP);
+        double* AP = vec(s, VAP);
+        for (int k = t; k < n; k += PC_T) {
+          const int4 nb = lay.nbr[k];
+          const double ap = row_apply(vec(s, VS)[k], vec(s, VW)[k], vec(s, VD)[k], vec(s, VE)[k], vec(s, VN)[k],
+                                      nb.x >= 0 ? P[nb.x] : 0.0, nb.y >= 0 ? P[nb.y] : 0.0, P[k],
+                                      nb.z >= 0 ? P[nb.z] : 0.0, nb.w >= 0 ? P[nb.w] : 0.0);
+          AP[k] = ap;
+          part[s] = fma(P[k], ap, part[s]);
+        }
+      }
+      pc_block_sums<S>(part, red, warp, lane);
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        if (!act[s]) continue;
+        if (!(part[s] > 0.0)) {
+          st[s] = VQPC_S_BREAKDOWN;
+          act[s] = false;
+          continue;
+        }
+        alpha[s] = rz[s] / part[s];
+        double* X = vec(s, VX);
+        double* R = vec(s, VR);
+        const double* P = vec(s, VP);
+        const double* AP = vec(s, VAP);
+        for (int k = t; k < n; k += PC_T) {
+          X[k] = __dadd_rn(X[k], __dmul_rn(alpha[s], P[k]));
+          R[k] = __dsub_rn(R[k], __dmul_rn(alpha[s], AP[k]));
+        }
+      }
+      __syncthreads();
+      // true residual b - A x (solver.cpp:220-222)
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        part[s] = 0.0;
+        if (!act[s]) continue;
+        const double* X = vec(s, VX);
+        for (int k = t; k < n; k += PC_T) {
+          const int4 nb = lay.nbr[k];
+          const double ax = row_apply(vec(s, VS)[k], vec(s, VW)[k], vec(s, VD)[k], vec(s, VE)[k], vec(s, VN)[k],
+                                      nb.x >= 0 ? X[nb.x] : 0.0, nb.y >= 0 ? X[nb.y] : 0.0, X[k],
+                                      nb.z >= 0 ? X[nb.z] : 0.0, nb.w >= 0 ? X[nb.w] : 0.0);
+          const double rt = __dsub_rn(vec(s, VB)[k], ax);
+          part[s] = fma(rt, rt, part[s]);
+        }
+      }
+      pc_block_sums<S>(part, red, warp, lane);
+      bool need = false;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        if (!act[s]) continue;
+        const double rel = sqrt(part[s]) / norm_b[s];
+        J[s] = j;
+        rel_rec[s] = rel;
+        if (rel < prm.eps) {
+          st[s] = VQPC_S_CONVERGED;
+          act[s] = false;
+        } else {
+          need = true;
+        }
+      }
+      if (!need) break;
+      solve(rzp);
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        if (!act[s]) continue;
+        if (!(rzp[s] > 0.0)) {
+          st[s] = VQPC_S_BREAKDOWN;
+          act[s] = false;
+          continue;
+        }
+        beta[s] = rzp[s] / rz[s];
+        rz[s] = rzp[s];
+        if (j >= mit[s]) act[s] = false;  // loop exhausted: MAX_ITER
+      }
+    }
+    // ---- outputs -------------------------------------------------------------------
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      if (s >= gr.y) continue;
+      if (t == 0) {
+        prm.iters[gsv[s]] = J[s];
+        prm.rel[gsv[s]] = rel_rec[s];
+        prm.status[gsv[s]] = st[s];
+      }
+      const bool solved = st[s] == VQPC_S_CONVERGED || st[s] == VQPC_S_MAX_ITER || st[s] == VQPC_S_BREAKDOWN;
+      if (prm.x_out && solved) {
+        double* xo = prm.x_out + static_cast<size_t>(gsv[s]) * n;
+        const double* X = vec(s, VX);
+        for (int k = t; k < n; k += PC_T) xo[lay.cperm[k]] = J[s] > 0 ? X[k] : 0.0;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Preconditioner::apply for one centroid in the oracle's serial order (tests):
+// y = L^-1 P r row by row, then L^T z = y column by column (one thread).
+__global__ void cholapply_serial_kernel(const double* L, int64_t ldL, const CholLayout lay, int p,
+                                        const double* r, double* y, double* z) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double* Lp = L + static_cast<size_t>(p) * ldL;
+  const int n = lay.n;
+  for (int k = 0; k < n; ++k) y[k] = r[lay.cperm[k]];
+  for (int k = 0; k < n; ++k) {
+    const int f = lay.first[k];
+    const double* Lk = Lp + lay.start[k] - f;
+    double s = y[k];
+    for (int j = f; j < k; ++j) s = __dsub_rn(s, __dmul_rn(y[j], Lk[j]));
+    y[k] = __ddiv_rn(s, Lk[k]);
+  }
+  for (int k = n - 1; k >= 0; --k) {
+    const int f = lay.first[k];
+    const double* Lk = Lp + lay.start[k] - f;
+    const double zk = __ddiv_rn(y[k], Lk[k]);
+    y[k] = zk;
+    for (int j = f; j < k; ++j) y[j] = __dsub_rn(y[j], __dmul_rn(Lk[j], zk));
+  }
+  for (int k = 0; k < n; ++k) z[lay.cperm[k]] = y[k];
+}
+
+}  // namespace vqpc

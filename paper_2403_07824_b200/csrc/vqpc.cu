@@ -25,6 +25,7 @@
 #include "pcg1d.cuh"
 #include "pcg1d_exact.cuh"
 #include "pcg2d.cuh"
+#include "pcgchol2d.cuh"
 #include "realise.cuh"
 #include "vqpc.h"
 
@@ -101,6 +102,18 @@ struct vqpc_ctx {
   DBuf<int> gmap;
   DBuf<double> bvec2;  // per-node right-hand side when it is not uniform (see pcg2d.cuh)
   DBuf<double> cnorm;  // |c_p|^2 for the contraction form of the assignment (assign_mma.cuh)
+  // 2-D `cholesky` preconditioner (pcgchol2d.cuh): RCM envelope, factors, groups
+  bool chol2d = false;
+  CholLayout clay{};
+  DBuf<int> ch_cperm, ch_first, ch_ngroups;
+  DBuf<int64_t> ch_start, ch_off;
+  DBuf<int4> ch_nbr;
+  DBuf<int2> ch_groups;
+  DBuf<int32_t> ch_perm;
+  DBuf<double> ch_L, ch_Linv, ch_work;
+  int64_t ch_ldL = 0, ch_ldLi = 0;
+  int ch_cap = 0;
+  int ch_S = 4;
   cudaStream_t aux = nullptr;              // chunks beyond the solve subset (overlap with the PCG)
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   DBuf<int> aflag;     // assign_mma candidate-list overflow flag
@@ -367,9 +380,81 @@ void run_schedule(vqpc_ctx* c, const double* d_xi, int64_t ld, const int32_t* d_
   (void)P;
 }
 
+size_t pchol_smem(const vqpc_ctx* c, int S) {
+  return sizeof(double) * (2 * (static_cast<size_t>(c->ch_cap) + PC_BS * PC_BS) + static_cast<size_t>(S) * PC_RING);
+}
+
+// 2-D `cholesky` kind: label-major order (stable over the cost-ordered queue), work
+// groups of up to S same-label samples, then one CTA per SM over the groups.
+void run_pcgchol2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d_kflag, const int32_t* d_perm,
+                   const int32_t* d_labels, int64_t B, int64_t out_base, double eps, int max_iter,
+                   const int32_t* d_mia, int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x,
+                   int64_t solve_limit) {
+  if (c->exact) throw ApiError{VQPC_INVALID_CONFIG, "reference-order mode is not available for the 2-D cholesky kind"};
+  const int P = c->pb.P, S = c->ch_S, n = c->n;
+  c->ch_perm.ensure(B);
+  c->ch_off.ensure(P + 2);
+  c->ch_groups.ensure(B + P + 1);
+  c->ch_ngroups.ensure(1);
+  {
+    Timed tm(c, VQPC_K_BUCKET);
+    counting_sort(c, d_labels, d_perm, B, P, c->ch_perm.p, c->ch_off.p);
+    chol_groups_kernel<<<1, 1, 0, c->stream>>>(c->ch_off.p, P, S, c->ch_groups.p, c->ch_ngroups.p);
+    launch_check(c);
+  }
+  void (*kern)(const PcholParams) = S == 1   ? pcgchol2d_kernel<1>
+                                    : S == 2 ? pcgchol2d_kernel<2>
+                                    : S == 3 ? pcgchol2d_kernel<3>
+                                             : pcgchol2d_kernel<4>;
+  const size_t smem = pchol_smem(c, S);
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PC_T, smem));
+  if (per_sm < 1) throw ApiError{VQPC_CUDA_ERROR, "pcgchol2d kernel does not fit on an SM"};
+  const int64_t blocks = cap_groups(std::min<int64_t>(ceil_div(B, S) + P + 1, static_cast<int64_t>(per_sm) * c->sm_count));
+  c->ch_work.ensure(static_cast<size_t>(blocks) * S * PC_NV * n);
+  c->counter.ensure(1);
+  CK(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->stream));
+  PcholParams prm{};
+  prm.g = c->g2;
+  prm.lay = c->clay;
+  prm.kappa = d_kappa;
+  prm.ldk = ldk;
+  prm.kflag = d_kflag;
+  prm.perm = c->ch_perm.p;
+  prm.labels = d_labels;
+  prm.groups = c->ch_groups.p;
+  prm.ngroups = c->ch_ngroups.p;
+  prm.L = c->ch_L.p;
+  prm.ldL = c->ch_ldL;
+  prm.Linv = c->ch_Linv.p;
+  prm.ldLi = c->ch_ldLi;
+  prm.cap = c->ch_cap;
+  prm.work = c->ch_work.p;
+  prm.B = B;
+  prm.out_base = out_base;
+  prm.solve_limit = solve_limit;
+  prm.eps = eps;
+  prm.max_iter = max_iter;
+  prm.max_iter_arr = d_mia;
+  prm.counter = c->counter.p;
+  prm.iters = d_iters;
+  prm.rel = d_rel;
+  prm.status = d_status;
+  prm.x_out = d_x;
+  Timed tm(c, VQPC_K_PCG);
+  kern<<<static_cast<unsigned>(blocks), PC_T, smem, c->stream>>>(prm);
+  launch_check(c);
+}
+
 void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d_kflag, const int32_t* d_perm,
                const int32_t* d_labels, int64_t B, int64_t out_base, double eps, int max_iter, const int32_t* d_mia,
                int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x, int64_t solve_limit) {
+  if (c->chol2d) {
+    run_pcgchol2d(c, d_kappa, ldk, d_kflag, d_perm, d_labels, B, out_base, eps, max_iter, d_mia, d_iters, d_rel,
+                  d_status, d_x, solve_limit);
+    return;
+  }
   int per_sm = 0;
   // C4's mesh (m = 255) has a specialised instantiation; other sizes take the generic one
   void (*kern)(const Pcg2dParams) = c->g2.m == 255 ? pcg2d_kernel<255> : pcg2d_kernel<0>;
@@ -630,6 +715,105 @@ void d2h(vqpc_ctx* c, T* dst, const T* src, size_t count) {
 
 int64_t kappa_ld(const vqpc_ctx* c) { return (c->pb.n_nodes + 1) & ~1; }
 
+// 2-D `cholesky` kind: the symbolic part, once per context (the pattern is the same
+// for every centroid and sample). Interior node id = iy * m + ix (fem.cpp:28-42);
+// its stored columns, ascending, are SW, S, W, itself, E, N, NE (the a-d diagonal of
+// every cell couples SW/NE with an exact zero the reference still stores, so they
+// count for the degrees and the envelope). Reverse Cuthill-McKee as in
+// solver.cpp:32-70: start every component at the unvisited node of least (degree,
+// id), breadth-first, each node's unvisited neighbours enqueued by (degree, id),
+// then the order reversed. Then the envelope of the permuted matrix (first[k] =
+// smallest permuted column of row k), its row offsets, and the staging capacity of
+// the blocked solves.
+void setup_chol2d(vqpc_ctx* c) {
+  const int m = c->g2.m, n = m * m;
+  auto cols = [&](int id, int* out) {  // ascending stored columns of row id
+    const int ix = id % m, iy = id / m;
+    int k = 0;
+    if (iy > 0 && ix > 0) out[k++] = id - m - 1;
+    if (iy > 0) out[k++] = id - m;
+    if (ix > 0) out[k++] = id - 1;
+    out[k++] = id;
+    if (ix < m - 1) out[k++] = id + 1;
+    if (iy < m - 1) out[k++] = id + m;
+    if (iy < m - 1 && ix < m - 1) out[k++] = id + m + 1;
+    return k;
+  };
+  std::vector<int> deg(n);
+  int buf[7];
+  for (int i = 0; i < n; ++i) deg[i] = cols(i, buf);
+  auto before = [&](int a, int b) { return deg[a] < deg[b] || (deg[a] == deg[b] && a < b); };
+  std::vector<int> seeds(n);
+  for (int i = 0; i < n; ++i) seeds[i] = i;
+  std::sort(seeds.begin(), seeds.end(), before);
+  std::vector<int> order;
+  order.reserve(n);
+  std::vector<char> visited(n, 0);
+  for (int s0 : seeds) {
+    if (visited[s0]) continue;
+    visited[s0] = 1;
+    size_t head = order.size();
+    order.push_back(s0);
+    while (head < order.size()) {
+      const int u = order[head++];
+      int nb[7], cnt = 0;
+      const int kk = cols(u, buf);
+      for (int e = 0; e < kk; ++e)
+        if (buf[e] != u && !visited[buf[e]]) {
+          visited[buf[e]] = 1;
+          nb[cnt++] = buf[e];
+        }
+      std::sort(nb, nb + cnt, before);
+      for (int e = 0; e < cnt; ++e) order.push_back(nb[e]);
+    }
+  }
+  std::reverse(order.begin(), order.end());  // order[k] = natural id of permuted row k
+  std::vector<int> inv(n), first(n);
+  for (int k = 0; k < n; ++k) inv[order[k]] = k;
+  std::vector<int64_t> start(n + 1, 0);
+  std::vector<int4> nbr(n);
+  int W = 0;
+  for (int k = 0; k < n; ++k) {
+    const int id = order[k], kk = cols(id, buf);
+    int f = k;
+    for (int e = 0; e < kk; ++e) f = std::min(f, inv[buf[e]]);
+    first[k] = f;
+    W = std::max(W, k - f);
+    start[k + 1] = start[k] + (k - f + 1);
+    const int ix = id % m, iy = id / m;
+    nbr[k] = make_int4(iy > 0 ? inv[id - m] : -1, ix > 0 ? inv[id - 1] : -1, ix < m - 1 ? inv[id + 1] : -1,
+                       iy < m - 1 ? inv[id + m] : -1);
+  }
+  const int nblk = static_cast<int>(ceil_div(n, PC_BS));
+  int64_t cap = 0;
+  for (int b = 0; b < nblk; ++b) {
+    const int r0 = b * PC_BS, r1 = std::min(n, r0 + PC_BS);
+    cap = std::max(cap, ((start[r1] + 1) & ~int64_t{1}) - (start[r0] & ~int64_t{1}));
+  }
+  if (W + 2 * PC_BS > PC_RING) throw ApiError{VQPC_INVALID_CONFIG, "cholesky envelope wider than the solve ring"};
+  c->ch_cperm.ensure(n);
+  c->ch_first.ensure(n);
+  c->ch_start.ensure(n + 1);
+  c->ch_nbr.ensure(n);
+  h2d(c, c->ch_cperm.p, order.data(), n);
+  h2d(c, c->ch_first.p, first.data(), n);
+  h2d(c, c->ch_start.p, start.data(), n + 1);
+  h2d(c, c->ch_nbr.p, nbr.data(), n);
+  c->clay.n = n;
+  c->clay.W = W;
+  c->clay.nblk = nblk;
+  c->clay.cperm = c->ch_cperm.p;
+  c->clay.first = c->ch_first.p;
+  c->clay.start = c->ch_start.p;
+  c->clay.nbr = c->ch_nbr.p;
+  c->ch_ldL = (start[n] + 1) & ~int64_t{1};
+  c->ch_ldLi = static_cast<int64_t>(nblk) * PC_BS * PC_BS;
+  c->ch_cap = static_cast<int>(cap);
+  c->chol2d = true;
+  if (const char* e = getenv("VQPC_CHOL_S")) c->ch_S = std::max(1, std::min(PC_MAXS, atoi(e)));
+  CK(cudaStreamSynchronize(c->stream));
+}
+
 // The full campaign on device-resident arrays (run_campaign_with semantics).
 void campaign_device(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, double eps, int max_iter, int64_t chunk,
                      int32_t* d_labels, int32_t* d_iters, double* d_rel, uint8_t* d_status, int64_t* d_stats,
@@ -780,7 +964,8 @@ int vqpc_ctx_create(const vqpc_problem* pb, vqpc_ctx** out) {
   const bool grid = pb->method == VQPC_GRID || pb->method == VQPC_SIGN_GRID;
   if (grid && !pb->latent) return VQPC_INVALID_CODEBOOK;
   if (pb->dim == 1 && pb->precond != VQPC_PC_CHOLESKY) return VQPC_INVALID_CONFIG;
-  if (pb->dim == 2 && (pb->precond != VQPC_PC_IC0 || pb->size - 1 > P2_T)) return VQPC_INVALID_CONFIG;
+  if (pb->dim == 2 && ((pb->precond != VQPC_PC_IC0 && pb->precond != VQPC_PC_CHOLESKY) || pb->size - 1 > P2_T))
+    return VQPC_INVALID_CONFIG;
   auto* c = new vqpc_ctx();
   c->pb = *pb;
   c->n = pb->dim == 1 ? pb->size - 1 : (pb->size - 1) * (pb->size - 1);
@@ -799,6 +984,7 @@ int vqpc_ctx_create(const vqpc_problem* pb, vqpc_ctx** out) {
       unsigned char dp[16][6];
       diag_orders(dp);
       CK(cudaMemcpyToSymbol(vqpc_dperm, dp, sizeof(dp)));
+      if (pb->precond == VQPC_PC_CHOLESKY) setup_chol2d(c);
     }
     if (pb->dim == 1) {
       const PcgVariant* v = pick_pcg(c->n);
@@ -857,6 +1043,13 @@ void vqpc_ctx_destroy(vqpc_ctx* c) {
   c->gmap.release();
   c->bvec2.release();
   c->cnorm.release();
+  for (auto* b : {&c->ch_cperm, &c->ch_first, &c->ch_ngroups}) b->release();
+  c->ch_start.release();
+  c->ch_off.release();
+  c->ch_nbr.release();
+  c->ch_groups.release();
+  c->ch_perm.release();
+  for (auto* b : {&c->ch_L, &c->ch_Linv, &c->ch_work}) b->release();
   if (c->aux) cudaStreamDestroy(c->aux);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
@@ -920,7 +1113,18 @@ int vqpc_factor_centroids(vqpc_ctx* c) {
     run_realise(c, c->xi.p, P, std::max(m, 1), m, c->kappa_c.p, ldk, c->kflag.p);
     c->err.ensure(1);
     CK(cudaMemsetAsync(c->err.p, 0, sizeof(int), c->stream));
-    if (pb.dim == 2) {
+    if (pb.dim == 2 && c->chol2d) {
+      c->ch_L.ensure(static_cast<size_t>(P) * c->ch_ldL);
+      c->ch_Linv.ensure(static_cast<size_t>(P) * c->ch_ldLi);
+      Timed tm(c, VQPC_K_OTHER);
+      cholfactor2d_kernel<<<P, PC_T, 0, c->stream>>>(c->kappa_c.p, ldk, P, c->g2, c->clay, c->ch_L.p, c->ch_ldL,
+                                                     c->err.p);
+      launch_check(c);
+      const int64_t th = static_cast<int64_t>(P) * c->clay.nblk * PC_BS;
+      cholinv_kernel<<<static_cast<unsigned>(ceil_div(th, 128)), 128, 0, c->stream>>>(c->ch_L.p, c->ch_ldL, c->clay,
+                                                                                      P, c->ch_Linv.p, c->ch_ldLi);
+      launch_check(c);
+    } else if (pb.dim == 2) {
       c->fac2.ensure(static_cast<size_t>(P) * P2_FAC * c->n);
       Timed tm(c, VQPC_K_OTHER);
       factor2d_kernel<<<P, P2_T, 0, c->stream>>>(c->kappa_c.p, ldk, P, c->g2, c->fac2.p, c->err.p);
@@ -966,7 +1170,10 @@ int vqpc_precond_apply(vqpc_ctx* c, int p, const double* r, double* z) {
     if (p < 0 || p >= c->pb.P) throw ApiError{VQPC_INVALID_ARGUMENT, "p out of range"};
     c->dvec.ensure(3 * static_cast<size_t>(c->n));
     h2d(c, c->dvec.p, r, c->n);
-    if (c->pb.dim == 2)
+    if (c->chol2d)
+      cholapply_serial_kernel<<<1, 1, 0, c->stream>>>(c->ch_L.p, c->ch_ldL, c->clay, p, c->dvec.p,
+                                                      c->dvec.p + 2 * c->n, c->dvec.p + c->n);
+    else if (c->pb.dim == 2)
       precond2d_apply_kernel<<<1, P2_T, 0, c->stream>>>(c->fac2.p, p, c->g2, c->dvec.p, c->dvec.p + c->n,
                                                         c->dvec.p + 2 * c->n);
     else
