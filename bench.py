@@ -73,7 +73,8 @@ def workload(cfg, B, K):
     else:
         r = cfg["mesh_resolution"]
         model = f"2-D P1 FEM on a {r}x{r} right-triangle mesh, {n} unknowns"
-        pc = "IC(0)"
+        pc = ("IC(0)" if cfg.get("precond") == "ic0"
+              else f"RCM + envelope Cholesky, {chol_rhs()} same-label samples per factor pass")
         kap = B * (r + 1) ** 2 * 8
     solve = f", PCG on the first {sub} samples" if sub else ""
     chunk = f", chunks of {cfg['chunk']}" if cfg.get("chunk") else ""
@@ -222,6 +223,18 @@ def roofline(cfg, prof, total_iters, B, steps, device):
             traffic = json.load(open(summ)).get(cfg["name"], {}).get("dram_bytes_per_launch")
         except (OSError, ValueError, AttributeError):
             traffic = None
+    if kind == "pcg" and cfg["dim"] == 2 and cfg.get("precond") == "cholesky":
+        nnz, S = cfg["_factor_entries"], chol_rhs()
+        work = (16.0 * nnz / S + 8.0 * (2 * npts + 14 * n)) * total_iters / lps
+        peak = measured_peaks().get("hbm_gbs")
+        achieved = work / (ms / 1e3) / 1e9
+        return {"kernel": "pcgchol2d", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if peak else None, "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, this pool's B200s)",
+                "algorithmic": f"(16 nnz(L) / S + 8 (2 N_nodes + 14 n)) bytes per PCG iteration x sum of J: the "
+                               f"envelope factor (nnz(L) = {nnz}) streamed forward and backward once per S = {S} "
+                               f"same-label right-hand sides, plus the IC(0) path's vector traffic",
+                "ms_per_launch": ms}
     if kind == "pcg" and cfg["dim"] == 2:
         work = 8.0 * (2 * npts + 14 * n) * total_iters / lps
         peak = measured_peaks().get("hbm_gbs")
@@ -250,6 +263,11 @@ def roofline(cfg, prof, total_iters, B, steps, device):
             "peak_source": "measured on this device: vqpc_fp64_peak DFMA-throughput probe "
                            "(MEASURED_PEAKS.json has no fp64 entry)",
             "algorithmic": what, "ms_per_launch": ms}
+
+
+def chol_rhs():
+    """Right-hand sides per factor pass of the 2-D cholesky kernel (VQPC_CHOL_S, default 4)."""
+    return max(1, min(4, int(os.environ.get("VQPC_CHOL_S", "4"))))
 
 
 def dgemm_peak(dev, n=8192, reps=3):
@@ -284,6 +302,9 @@ def kernel_rooflines(cfg, prof, total_iters, B, K, steps, peaks):
     work = {}
     if cfg["dim"] == 1:
         work["pcg"] = (31.0 * n * total_iters / 1e12, "TFLOP/s", "fp64")
+    elif cfg.get("precond") == "cholesky":
+        work["pcg"] = ((16.0 * cfg["_factor_entries"] / chol_rhs() + 8.0 * (2 * npts + 14 * n)) * total_iters / 1e9,
+                       "GB/s", "hbm")
     else:
         work["pcg"] = (8.0 * (2 * npts + 14 * n) * total_iters / 1e9, "GB/s", "hbm")
     work["realise"] = (2.0 * npts * K * B / 1e12, "TFLOP/s", "dgemm")
@@ -343,6 +364,7 @@ def run_ours(args, rank, world, local_rank):
                          rel=torch.empty(B, dtype=torch.float64, device=dev),
                          st=torch.empty(B, dtype=torch.uint8, device=dev),
                          stats=torch.empty(4 * P + 4, dtype=torch.int64, device=dev)))
+    cfg = dict(cfg, _factor_entries=ctxs[0].factor_entries)
 
     coll = {"last": None}  # event after the previous step's all-reduce
 

@@ -116,6 +116,9 @@ int vqpc_set_exact_reductions(vqpc_ctx* ctx, int enable);
 /* unknowns per sample system (n) and the number of device kernel launches
  * issued by this context so far (bench evidence). */
 int vqpc_unknowns(const vqpc_ctx* ctx);
+/* stored entries of one centroid's factor: 1-D tridiagonal 2n - 1, 2-D IC(0) 3n
+ * (D, a_W, a_S), 2-D cholesky the RCM envelope of L (roofline accounting). */
+int64_t vqpc_factor_entries(const vqpc_ctx* ctx);
 int64_t vqpc_launch_count(const vqpc_ctx* ctx);
 
 /* ---- (e) centroid factors: centroid_coefficient -> assemble -> build_cholesky

@@ -35,6 +35,12 @@ constexpr int PC_BS = 32;     // rows per block of the triangular solves
 constexpr int PC_RING = 1024; // y / w ring (rows)
 constexpr int PC_NV = 11;     // per sample slot: D, cS, cW, cE, cN, b, x, r, p, Ap, z
 constexpr int PC_MAXS = 4;
+// per block of a centroid's Linv array and of a stage (doubles): Linv_B [1024] |
+// block metadata [32: first[32], offset of row i's column 0 in the staged rows[32]];
+// a stage then holds the block's envelope rows
+constexpr int PC_STG_META = PC_BS * PC_BS;
+constexpr int PC_LIB = PC_STG_META + PC_BS;
+constexpr int PC_STG_R = PC_LIB;
 
 struct CholLayout {
   int n;                 // unknowns
@@ -93,7 +99,8 @@ __global__ void __launch_bounds__(PC_T) cholfactor2d_kernel(const double* kappa_
 }
 
 // inverse of every 32 x 32 diagonal block of L (row-major [i][c], zero above the
-// diagonal; rows past n are identity rows). One thread per (centroid, block, column).
+// diagonal; rows past n are identity rows), into the first 1024 doubles of the
+// block's PC_LIB-double record. One thread per (centroid, block, column).
 __global__ void cholinv_kernel(const double* L, int64_t ldL, const CholLayout lay, int P, double* Linv,
                                int64_t ldLi) {
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -103,7 +110,7 @@ __global__ void cholinv_kernel(const double* L, int64_t ldL, const CholLayout la
   const int p = static_cast<int>(bp / lay.nblk), blk = static_cast<int>(bp % lay.nblk);
   const int r0 = blk * PC_BS;
   const double* Lp = L + static_cast<size_t>(p) * ldL;
-  double* out = Linv + static_cast<size_t>(p) * ldLi + static_cast<size_t>(blk) * PC_BS * PC_BS;
+  double* out = Linv + static_cast<size_t>(p) * ldLi + static_cast<size_t>(blk) * (PC_BS * PC_BS + PC_BS);
   double x[PC_BS];
   for (int i = 0; i < PC_BS; ++i) {
     const int k = r0 + i;
@@ -157,7 +164,10 @@ struct PcholParams {
   const double* Linv;   // P x ldLi inverted diagonal blocks
   int64_t ldLi;
   int cap;              // doubles per staged block (max over blocks, 16-byte padded)
-  double* work;         // per CTA: S * PC_NV * n doubles
+  const int64_t* blk_a0;     // per block: first staged L index (even)
+  const unsigned* blk_bytes; // per block: staged bytes (multiple of 16)
+  int ldv;              // per-slot vector stride (multiple of 32)
+  double* work;         // per CTA: S * PC_NV * ldv doubles
   int64_t B, out_base, solve_limit;
   double eps;
   int max_iter;
@@ -222,7 +232,7 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
   const Grid2D g = prm.g;
   const CholLayout lay = prm.lay;
   const int n = lay.n, t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int stage_len = prm.cap + PC_BS * PC_BS;
+  const int stage_len = PC_LIB + prm.cap;
   double* ring = dsm + 2 * stage_len;  // [S][PC_RING]
   const unsigned bar0 = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[0]));
   if (t == 0) {
@@ -231,8 +241,9 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  double* base = prm.work + static_cast<size_t>(blockIdx.x) * S * PC_NV * n;
-  auto vec = [&](int s, int v) { return base + (static_cast<size_t>(s) * PC_NV + v) * n; };
+  const int ldv = prm.ldv;  // vector stride: n rounded up to whole 32-row blocks (TMA-aligned)
+  double* base = prm.work + static_cast<size_t>(blockIdx.x) * S * PC_NV * ldv;
+  auto vec = [&](int s, int v) { return base + (static_cast<size_t>(s) * PC_NV + v) * ldv; };
   enum { VD = 0, VS, VW, VE, VN, VB, VX, VR, VP, VAP, VZ };
   int64_t vg = 0;  // staged-block visits issued by this CTA (mbarrier phases)
   const int nvis = 2 * lay.nblk;
@@ -304,71 +315,95 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
     for (int s = 0; s < S; ++s) norm_b[s] = sqrt(part[s]);
 
     // ---- z = M^{-1} r for every slot of the group; returns the r.z partials --------
-    auto issue = [&](int v) {
-      if (t != 0 || v >= nvis) return;
-      const int blk = v < lay.nblk ? v : nvis - 1 - v;
-      const int r0 = blk * PC_BS, r1 = min(n, r0 + PC_BS);
-      const int64_t a0 = lay.start[r0] & ~1ll, a1 = (lay.start[r1] + 1) & ~1ll;
-      const int64_t gv = vg + v;
-      const int stg = static_cast<int>(gv & 1);
+    // Visit v = 0 .. 2 nblk - 1 walks the blocks forward then backward. Everything a
+    // visit reads from HBM arrives by TMA one visit ahead on the stage's mbarrier:
+    // Linv_B, the block's metadata (first[], offsets), r_B of every slot, the block's
+    // envelope rows, and (backward) the y block entering the w window.
+    const int WB = (lay.W + PC_BS - 1) / PC_BS;
+    // issued by warp 0, one copy per lane (lane 0 arms the barrier first)
+    auto issue = [&](int v, int64_t a0, unsigned cbytes) {
+      if (warp != 0 || v >= nvis) return;
+      const bool fwd = v < lay.nblk;
+      const int blk = fwd ? v : nvis - 1 - v;
+      const int stg = static_cast<int>((vg + v) & 1);
       double* sp = dsm + stg * stage_len;
       const unsigned bar = bar0 + 8u * stg;
-      const unsigned cbytes = static_cast<unsigned>((a1 - a0) * 8);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      pc_mbar_expect(bar, cbytes + PC_BS * PC_BS * 8u);
-      pc_bulk_g2s(static_cast<unsigned>(__cvta_generic_to_shared(sp)),
-                  Lip + static_cast<size_t>(blk) * PC_BS * PC_BS, PC_BS * PC_BS * 8u, bar);
-      pc_bulk_g2s(static_cast<unsigned>(__cvta_generic_to_shared(sp + PC_BS * PC_BS)), Lp + a0, cbytes, bar);
+      const int e = blk - WB;  // backward: y block entering the window (not left in the ring by the forward sweep)
+      const bool zin = !fwd && e >= 0 && e < lay.nblk - PC_RING / PC_BS;
+      if (lane == 0) pc_mbar_expect(bar, PC_LIB * 8u + cbytes + (zin ? S * 256u : 0u));
+      __syncwarp();
+      auto sa = [](const void* q) { return static_cast<unsigned>(__cvta_generic_to_shared(q)); };
+      if (lane == 0) {
+        pc_bulk_g2s(sa(sp + PC_LIB), Lp + a0, cbytes, bar);
+      } else if (lane == 1) {
+        pc_bulk_g2s(sa(sp), Lip + static_cast<size_t>(blk) * PC_LIB, PC_LIB * 8u, bar);
+      } else if (zin && lane >= 8 && lane < 8 + S) {
+        const int s = lane - 8;
+        pc_bulk_g2s(sa(ring + s * PC_RING + ((e * PC_BS) & (PC_RING - 1))), vec(s, VZ) + e * PC_BS, 256u, bar);
+      }
     };
+    auto blk_of = [&](int v) { return v < lay.nblk ? v : nvis - 1 - v; };
     auto solve = [&](double (&rzp)[S]) {
+      P2_TIC(t_solve);
 #pragma unroll
       for (int s = 0; s < S; ++s) rzp[s] = 0.0;
       __syncthreads();
-      issue(0);
-      issue(1);
-      int init_lo = n;
+      if (warp == 0) {
+        issue(0, prm.blk_a0[blk_of(0)], prm.blk_bytes[blk_of(0)]);
+        if (nvis > 1) issue(1, prm.blk_a0[blk_of(1)], prm.blk_bytes[blk_of(1)]);
+      }
       for (int v = 0; v < nvis; ++v) {
         const bool fwd = v < lay.nblk;
-        const int blk = fwd ? v : nvis - 1 - v;
+        const int blk = blk_of(v);
         const int r0 = blk * PC_BS, r1 = min(n, r0 + PC_BS);
         const int64_t gv = vg + v;
         const int stg = static_cast<int>(gv & 1);
         const double* Li = dsm + stg * stage_len;
-        const double* ch = Li + PC_BS * PC_BS - (lay.start[r0] & ~1ll);  // ch[start-index] = L value
-        if (t < PC_BS) {
-          const int k = r0 + t;
-          s_first[t] = k < n ? lay.first[k] : k;
-          s_start[t] = k < n ? lay.start[k] : 0;
+        const int* meta = reinterpret_cast<const int*>(Li + PC_STG_META);  // first[32], off[32]
+        const double* ch = Li + PC_LIB;  // L(r0 + i, j) = ch[off[i] + j]
+        int64_t na0 = 0;
+        unsigned nby = 0;
+        if (warp == 0 && v + 2 < nvis) {  // next issue's source range, loaded while this visit computes
+          na0 = prm.blk_a0[blk_of(v + 2)];
+          nby = prm.blk_bytes[blk_of(v + 2)];
         }
+        // r of the rows this thread finishes (forward: row t >> 3 for q < S; backward:
+        // row t >> 3 of slot q), loaded before the wait so the latency hides behind it
+        double rv = 0.0;
+        {
+          const int ii = t >> 3, q = t & 7;
+          if (q < S && r0 + ii < r1) rv = vec(q, VR)[r0 + ii];
+        }
+        P2_TIC(t_wait);
+        pc_mbar_wait(bar0 + 8u * stg, static_cast<unsigned>((gv >> 1) & 1));
+        P2_TOC(2, t_wait);
+        P2_TIC(t_fwd);
         if (fwd) {
-          double rk[S][4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int k = r0 + 4 * warp + i;
-#pragma unroll
-            for (int s = 0; s < S; ++s) rk[s][i] = (lane == 0 && k < r1) ? vec(s, VR)[k] : 0.0;
-          }
-          __syncthreads();
-          pc_mbar_wait(bar0 + 8u * stg, static_cast<unsigned>((gv >> 1) & 1));
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int ii = 4 * warp + i, k = r0 + ii;
+          {
+            const int ii = t >> 3, q = t & 7;
             double acc[S];
 #pragma unroll
             for (int s = 0; s < S; ++s) acc[s] = 0.0;
-            if (k < r1) {
-              const int f = s_first[ii];
-              const double* row = ch + (s_start[ii] - f);
-              for (int j = f + lane; j < r0; j += 32) {
-                const double lv = row[j];
+            const int f = meta[ii], off = meta[PC_BS + ii];
+            const int cofs = static_cast<int>(ch - dsm);  // staged rows, as an index into dsm
+#pragma unroll 2
+            for (int j = f + q; j < r0; j += 8) {
+              const double lv = dsm[cofs + off + j];
+              const int rj = j & (PC_RING - 1);
 #pragma unroll
-                for (int s = 0; s < S; ++s) acc[s] = fma(lv, ring[s * PC_RING + (j & (PC_RING - 1))], acc[s]);
-              }
+              for (int s = 0; s < S; ++s) acc[s] = fma(lv, ring[s * PC_RING + rj], acc[s]);
             }
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-              acc[s] = warp_allsum(acc[s]);
-              if (lane == 0) tv[s][ii] = k < r1 ? rk[s][i] - acc[s] : 0.0;
+              acc[s] += shfl_xor(acc[s], 1);
+              acc[s] += shfl_xor(acc[s], 2);
+              acc[s] += shfl_xor(acc[s], 4);
+            }
+            if (q < S) {
+              double a = acc[0];
+#pragma unroll
+              for (int s = 1; s < S; ++s) a = q == s ? acc[s] : a;
+              tv[q][ii] = r0 + ii < r1 ? rv - a : 0.0;
             }
           }
           __syncthreads();
@@ -386,16 +421,12 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
               vec(s, VZ)[r0 + i] = y;
             }
           }
+          // y goes back to HBM; the backward sweep re-reads blocks of it by TMA, the
+          // first of them WB + 1 visits after the sweep turns (fence below)
           __syncthreads();
+          P2_TOC(3, t_fwd);
         } else {
-          // w ring: rows entering the window take their y
-          const int new_lo = r0 - lay.W > 0 ? r0 - lay.W : 0;
-          for (int j = new_lo + t; j < init_lo; j += PC_T)
-#pragma unroll
-            for (int s = 0; s < S; ++s) ring[s * PC_RING + (j & (PC_RING - 1))] = vec(s, VZ)[j];
-          init_lo = new_lo < init_lo ? new_lo : init_lo;
-          __syncthreads();
-          pc_mbar_wait(bar0 + 8u * stg, static_cast<unsigned>((gv >> 1) & 1));
+          if (v == lay.nblk) asm volatile("fence.proxy.async;" ::: "memory");  // this thread's y stores
           const int c = t >> 3, q = t & 7;
 #pragma unroll
           for (int s = 0; s < S; ++s) {
@@ -411,35 +442,37 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
             z += shfl_xor(z, 4);
             if (q == 0) {
               tv[s][c] = r0 + c < r1 ? z : 0.0;
-              if (r0 + c < r1) {
-                vec(s, VZ)[r0 + c] = z;
-                rzp[s] = fma(vec(s, VR)[r0 + c], z, rzp[s]);
-              }
+              if (r0 + c < r1) vec(s, VZ)[r0 + c] = z;
             }
+            if (q == s && r0 + c < r1) rzp[s] = fma(rv, z, rzp[s]);
           }
           __syncthreads();
-          for (int j = new_lo + t; j < r0; j += PC_T) {
+          const int lo = r0 - lay.W > 0 ? r0 - lay.W : 0;
+          const int cofs = static_cast<int>(ch - dsm);
+          for (int j = lo + t; j < r0; j += PC_T) {
             double acc[S];
 #pragma unroll
             for (int s = 0; s < S; ++s) acc[s] = 0.0;
-#pragma unroll 4
-            for (int i = 0; i < r1 - r0; ++i) {
-              const int f = s_first[i];
-              if (j >= f) {
-                const double lv = ch[s_start[i] - f + j];
+#pragma unroll 8
+            for (int i = 0; i < PC_BS; ++i) {
+              // entries left of first[] read a neighbouring row's value (still inside
+              // the stage) and are zeroed; rows past n have first = k > j
+              const double lv = j >= meta[i] ? dsm[cofs + meta[PC_BS + i] + j] : 0.0;
 #pragma unroll
-                for (int s = 0; s < S; ++s) acc[s] = fma(lv, tv[s][i], acc[s]);
-              }
+              for (int s = 0; s < S; ++s) acc[s] = fma(lv, tv[s][i], acc[s]);
             }
 #pragma unroll
             for (int s = 0; s < S; ++s) ring[s * PC_RING + (j & (PC_RING - 1))] -= acc[s];
           }
           __syncthreads();
         }
-        issue(v + 2);
+        P2_TIC(t_iss);
+        issue(v + 2, na0, nby);
+        P2_TOC(0, t_iss);
       }
       vg += nvis;
       pc_block_sums<S>(rzp, red, warp, lane);
+      P2_TOC(1, t_solve);
     };
 
     bool any0 = false;

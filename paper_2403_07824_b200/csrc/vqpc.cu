@@ -106,12 +106,14 @@ struct vqpc_ctx {
   bool chol2d = false;
   CholLayout clay{};
   DBuf<int> ch_cperm, ch_first, ch_ngroups;
-  DBuf<int64_t> ch_start, ch_off;
+  DBuf<int64_t> ch_start, ch_off, ch_a0;
+  DBuf<int> ch_bmeta;
+  DBuf<unsigned> ch_bytes;
   DBuf<int4> ch_nbr;
   DBuf<int2> ch_groups;
   DBuf<int32_t> ch_perm;
   DBuf<double> ch_L, ch_Linv, ch_work;
-  int64_t ch_ldL = 0, ch_ldLi = 0;
+  int64_t ch_ldL = 0, ch_ldLi = 0, ch_nnz = 0;
   int ch_cap = 0;
   int ch_S = 4;
   cudaStream_t aux = nullptr;              // chunks beyond the solve subset (overlap with the PCG)
@@ -381,7 +383,7 @@ void run_schedule(vqpc_ctx* c, const double* d_xi, int64_t ld, const int32_t* d_
 }
 
 size_t pchol_smem(const vqpc_ctx* c, int S) {
-  return sizeof(double) * (2 * (static_cast<size_t>(c->ch_cap) + PC_BS * PC_BS) + static_cast<size_t>(S) * PC_RING);
+  return sizeof(double) * (2 * (static_cast<size_t>(c->ch_cap) + PC_LIB) + static_cast<size_t>(S) * PC_RING);
 }
 
 // 2-D `cholesky` kind: label-major order (stable over the cost-ordered queue), work
@@ -412,7 +414,8 @@ void run_pcgchol2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PC_T, smem));
   if (per_sm < 1) throw ApiError{VQPC_CUDA_ERROR, "pcgchol2d kernel does not fit on an SM"};
   const int64_t blocks = cap_groups(std::min<int64_t>(ceil_div(B, S) + P + 1, static_cast<int64_t>(per_sm) * c->sm_count));
-  c->ch_work.ensure(static_cast<size_t>(blocks) * S * PC_NV * n);
+  const int ldv = static_cast<int>(ceil_div(n, PC_BS) * PC_BS);
+  c->ch_work.ensure(static_cast<size_t>(blocks) * S * PC_NV * ldv);
   c->counter.ensure(1);
   CK(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->stream));
   PcholParams prm{};
@@ -430,6 +433,9 @@ void run_pcgchol2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_
   prm.Linv = c->ch_Linv.p;
   prm.ldLi = c->ch_ldLi;
   prm.cap = c->ch_cap;
+  prm.blk_a0 = c->ch_a0.p;
+  prm.blk_bytes = c->ch_bytes.p;
+  prm.ldv = ldv;
   prm.work = c->ch_work.p;
   prm.B = B;
   prm.out_base = out_base;
@@ -785,12 +791,31 @@ void setup_chol2d(vqpc_ctx* c) {
                        iy < m - 1 ? inv[id + m] : -1);
   }
   const int nblk = static_cast<int>(ceil_div(n, PC_BS));
+  // per 32-row block: the staged range of L (16-byte aligned) and, per row, first[]
+  // and the offset of its column 0 inside the staged range (rows past n: empty)
   int64_t cap = 0;
+  std::vector<int64_t> a0s(nblk);
+  std::vector<unsigned> bytes(nblk);
+  std::vector<int> bmeta(static_cast<size_t>(nblk) * 2 * PC_BS);
   for (int b = 0; b < nblk; ++b) {
     const int r0 = b * PC_BS, r1 = std::min(n, r0 + PC_BS);
-    cap = std::max(cap, ((start[r1] + 1) & ~int64_t{1}) - (start[r0] & ~int64_t{1}));
+    const int64_t a0 = start[r0] & ~int64_t{1}, a1 = (start[r1] + 1) & ~int64_t{1};
+    cap = std::max(cap, a1 - a0);
+    a0s[b] = a0;
+    bytes[b] = static_cast<unsigned>((a1 - a0) * 8);
+    for (int i = 0; i < PC_BS; ++i) {
+      const int k = r0 + i;
+      bmeta[static_cast<size_t>(b) * 2 * PC_BS + i] = k < n ? first[k] : k;
+      bmeta[static_cast<size_t>(b) * 2 * PC_BS + PC_BS + i] = k < n ? static_cast<int>(start[k] - first[k] - a0) : 0;
+    }
   }
-  if (W + 2 * PC_BS > PC_RING) throw ApiError{VQPC_INVALID_CONFIG, "cholesky envelope wider than the solve ring"};
+  c->ch_a0.ensure(nblk);
+  c->ch_bytes.ensure(nblk);
+  c->ch_bmeta.ensure(bmeta.size());
+  h2d(c, c->ch_a0.p, a0s.data(), nblk);
+  h2d(c, c->ch_bytes.p, bytes.data(), nblk);
+  h2d(c, c->ch_bmeta.p, bmeta.data(), bmeta.size());
+  if (W + 3 * PC_BS > PC_RING) throw ApiError{VQPC_INVALID_CONFIG, "cholesky envelope wider than the solve ring"};
   c->ch_cperm.ensure(n);
   c->ch_first.ensure(n);
   c->ch_start.ensure(n + 1);
@@ -807,7 +832,8 @@ void setup_chol2d(vqpc_ctx* c) {
   c->clay.start = c->ch_start.p;
   c->clay.nbr = c->ch_nbr.p;
   c->ch_ldL = (start[n] + 1) & ~int64_t{1};
-  c->ch_ldLi = static_cast<int64_t>(nblk) * PC_BS * PC_BS;
+  c->ch_nnz = start[n];
+  c->ch_ldLi = static_cast<int64_t>(nblk) * PC_LIB;
   c->ch_cap = static_cast<int>(cap);
   c->chol2d = true;
   if (const char* e = getenv("VQPC_CHOL_S")) c->ch_S = std::max(1, std::min(PC_MAXS, atoi(e)));
@@ -949,6 +975,11 @@ const char* vqpc_error_string(int code) {
 
 const char* vqpc_last_error(const vqpc_ctx* c) { return c ? c->last_error.c_str() : ""; }
 int vqpc_unknowns(const vqpc_ctx* c) { return c ? c->n : 0; }
+int64_t vqpc_factor_entries(const vqpc_ctx* c) {
+  if (!c) return 0;
+  if (c->chol2d) return c->ch_nnz;
+  return c->pb.dim == 2 ? 3 * static_cast<int64_t>(c->n) : 2 * static_cast<int64_t>(c->n) - 1;
+}
 int64_t vqpc_launch_count(const vqpc_ctx* c) { return c ? c->launches : 0; }
 
 int vqpc_ctx_create(const vqpc_problem* pb, vqpc_ctx** out) {
@@ -1043,7 +1074,9 @@ void vqpc_ctx_destroy(vqpc_ctx* c) {
   c->gmap.release();
   c->bvec2.release();
   c->cnorm.release();
-  for (auto* b : {&c->ch_cperm, &c->ch_first, &c->ch_ngroups}) b->release();
+  for (auto* b : {&c->ch_cperm, &c->ch_first, &c->ch_ngroups, &c->ch_bmeta}) b->release();
+  c->ch_a0.release();
+  c->ch_bytes.release();
   c->ch_start.release();
   c->ch_off.release();
   c->ch_nbr.release();
@@ -1124,6 +1157,10 @@ int vqpc_factor_centroids(vqpc_ctx* c) {
       cholinv_kernel<<<static_cast<unsigned>(ceil_div(th, 128)), 128, 0, c->stream>>>(c->ch_L.p, c->ch_ldL, c->clay,
                                                                                       P, c->ch_Linv.p, c->ch_ldLi);
       launch_check(c);
+      for (int p = 0; p < P; ++p)  // each block record's metadata tail (one TMA copy per block)
+        CK(cudaMemcpy2DAsync(c->ch_Linv.p + static_cast<size_t>(p) * c->ch_ldLi + PC_STG_META, PC_LIB * sizeof(double),
+                             c->ch_bmeta.p, 2 * PC_BS * sizeof(int), 2 * PC_BS * sizeof(int), c->clay.nblk,
+                             cudaMemcpyDeviceToDevice, c->stream));
     } else if (pb.dim == 2) {
       c->fac2.ensure(static_cast<size_t>(P) * P2_FAC * c->n);
       Timed tm(c, VQPC_K_OTHER);

@@ -54,6 +54,7 @@ def load():
             "vqpc_synchronize": (I, [VP]),
             "vqpc_set_exact_reductions": (I, [VP, I]),
             "vqpc_unknowns": (I, [VP]),
+            "vqpc_factor_entries": (C.c_int64, [VP]),
             "vqpc_launch_count": (I64, [VP]),
             "vqpc_factor_centroids": (I, [VP]),
             "vqpc_centroid_coefficients": (I, [VP, VP]),
@@ -186,6 +187,7 @@ class Context:
         _check(load().vqpc_ctx_create(C.byref(pb), C.byref(h)))
         self.h = h
         self.n = load().vqpc_unknowns(h)
+        self.factor_entries = int(load().vqpc_factor_entries(h))
         self.factored = False
 
     def close(self):
