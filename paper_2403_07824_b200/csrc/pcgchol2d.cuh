@@ -35,6 +35,7 @@ constexpr int PC_BS = 32;     // rows per block of the triangular solves
 constexpr int PC_RING = 1024; // y / w ring (rows)
 constexpr int PC_NV = 11;     // per sample slot: D, cS, cW, cE, cN, b, x, r, p, Ap, z
 constexpr int PC_MAXS = 4;
+constexpr int PC_WIN = 256;   // columns left of a block the products cover (>= the envelope width W)
 // per block of a centroid's Linv array and of a stage (doubles): Linv_B [1024] |
 // block metadata [32: first[32], offset of row i's column 0 in the staged rows[32]];
 // a stage then holds the block's envelope rows
@@ -198,6 +199,12 @@ __device__ __forceinline__ void pc_mbar_wait(unsigned bar, unsigned parity) {
       : "memory");
 }
 
+__device__ __forceinline__ void pc_dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 template <int S>
 __device__ __forceinline__ void pc_block_sums(double (&v)[S], double (*red)[PC_T / 32], int warp, int lane) {
 #pragma unroll
@@ -226,6 +233,7 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
   __shared__ __align__(8) unsigned long long mbar[2];
   __shared__ double red[S][PC_T / 32];
   __shared__ double tv[S][PC_BS];
+  __shared__ double red2[(PC_T / 32) * PC_BS * S];  // per-warp partial products (forward)
   __shared__ int s_first[PC_BS];
   __shared__ int64_t s_start[PC_BS];
   __shared__ int s_grp;
@@ -380,29 +388,44 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
         P2_TIC(t_fwd);
         if (fwd) {
           {
+            // T = L_{B,window} Y on the fp64 tensor pipe (mma.sync.m8n8k4.f64): 32 rows
+            // (4 m-tiles) x the PC_WIN columns left of the block (8 k-steps per warp) x
+            // the S slots (N = 8, zero-padded); entries left of first[] are zeros
+            const int cofs = static_cast<int>(ch - dsm);
+            const int ra = lane >> 2, ka = lane & 3;
+            const int jw = r0 - PC_WIN + 32 * warp;
+            int fr[4], of[4];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+              fr[mt] = meta[8 * mt + ra];
+              of[mt] = cofs + meta[PC_BS + 8 * mt + ra];
+            }
+            double c[4][2];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) c[mt][0] = c[mt][1] = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+              const int j = jw + 4 * ks + ka;
+              const double b = (ra < S && j >= 0) ? ring[ra * PC_RING + (j & (PC_RING - 1))] : 0.0;
+#pragma unroll
+              for (int mt = 0; mt < 4; ++mt) {
+                const double a = j >= fr[mt] ? dsm[of[mt] + j] : 0.0;
+                pc_dmma(c[mt][0], c[mt][1], a, b);
+              }
+            }
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+              for (int e = 0; e < 2; ++e)
+                if (2 * ka + e < S) red2[(warp * PC_BS + 8 * mt + ra) * S + 2 * ka + e] = c[mt][e];
+          }
+          __syncthreads();
+          {
             const int ii = t >> 3, q = t & 7;
-            double acc[S];
-#pragma unroll
-            for (int s = 0; s < S; ++s) acc[s] = 0.0;
-            const int f = meta[ii], off = meta[PC_BS + ii];
-            const int cofs = static_cast<int>(ch - dsm);  // staged rows, as an index into dsm
-#pragma unroll 2
-            for (int j = f + q; j < r0; j += 8) {
-              const double lv = dsm[cofs + off + j];
-              const int rj = j & (PC_RING - 1);
-#pragma unroll
-              for (int s = 0; s < S; ++s) acc[s] = fma(lv, ring[s * PC_RING + rj], acc[s]);
-            }
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-              acc[s] += shfl_xor(acc[s], 1);
-              acc[s] += shfl_xor(acc[s], 2);
-              acc[s] += shfl_xor(acc[s], 4);
-            }
             if (q < S) {
-              double a = acc[0];
+              double a = 0.0;
 #pragma unroll
-              for (int s = 1; s < S; ++s) a = q == s ? acc[s] : a;
+              for (int w = 0; w < PC_T / 32; ++w) a += red2[(w * PC_BS + ii) * S + q];
               tv[q][ii] = r0 + ii < r1 ? rv - a : 0.0;
             }
           }
@@ -448,21 +471,35 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
           }
           __syncthreads();
           const int lo = r0 - lay.W > 0 ? r0 - lay.W : 0;
-          const int cofs = static_cast<int>(ch - dsm);
-          for (int j = lo + t; j < r0; j += PC_T) {
-            double acc[S];
+          {
+            // w_j -= sum_i L(r0 + i, j) z_i for the PC_WIN columns left of the block, as
+            // DMMA tiles: M = columns (4 m-tiles of 8 per warp), K = the 32 block rows
+            // (8 k-steps), N = the S slots
+            const int cofs = static_cast<int>(ch - dsm);
+            const int ra = lane >> 2, ka = lane & 3;
+            int fi[8], oi[8];
+            double bz[8];
 #pragma unroll
-            for (int s = 0; s < S; ++s) acc[s] = 0.0;
-#pragma unroll 8
-            for (int i = 0; i < PC_BS; ++i) {
-              // entries left of first[] read a neighbouring row's value (still inside
-              // the stage) and are zeroed; rows past n have first = k > j
-              const double lv = j >= meta[i] ? dsm[cofs + meta[PC_BS + i] + j] : 0.0;
-#pragma unroll
-              for (int s = 0; s < S; ++s) acc[s] = fma(lv, tv[s][i], acc[s]);
+            for (int ks = 0; ks < 8; ++ks) {
+              const int i = 4 * ks + ka;
+              fi[ks] = meta[i];
+              oi[ks] = cofs + meta[PC_BS + i];
+              bz[ks] = ra < S ? tv[ra][i] : 0.0;
             }
 #pragma unroll
-            for (int s = 0; s < S; ++s) ring[s * PC_RING + (j & (PC_RING - 1))] -= acc[s];
+            for (int mt = 0; mt < 4; ++mt) {
+              const int j = r0 - PC_WIN + 32 * warp + 8 * mt + ra;
+              double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+              for (int ks = 0; ks < 8; ++ks) {
+                const double a = j >= fi[ks] ? dsm[oi[ks] + j] : 0.0;
+                pc_dmma(c0, c1, a, bz[ks]);
+              }
+              if (j >= lo) {
+                if (2 * ka < S) ring[(2 * ka) * PC_RING + (j & (PC_RING - 1))] -= c0;
+                if (2 * ka + 1 < S) ring[(2 * ka + 1) * PC_RING + (j & (PC_RING - 1))] -= c1;
+              }
+            }
           }
           __syncthreads();
         }

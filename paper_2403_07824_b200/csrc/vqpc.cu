@@ -815,7 +815,7 @@ void setup_chol2d(vqpc_ctx* c) {
   h2d(c, c->ch_a0.p, a0s.data(), nblk);
   h2d(c, c->ch_bytes.p, bytes.data(), nblk);
   h2d(c, c->ch_bmeta.p, bmeta.data(), bmeta.size());
-  if (W + 3 * PC_BS > PC_RING) throw ApiError{VQPC_INVALID_CONFIG, "cholesky envelope wider than the solve ring"};
+  if (W > PC_WIN || W + 3 * PC_BS > PC_RING) throw ApiError{VQPC_INVALID_CONFIG, "cholesky envelope wider than the solve ring"};
   c->ch_cperm.ensure(n);
   c->ch_first.ensure(n);
   c->ch_start.ensure(n + 1);
