@@ -266,8 +266,8 @@ def roofline(cfg, prof, total_iters, B, steps, device):
 
 
 def chol_rhs():
-    """Right-hand sides per factor pass of the 2-D cholesky kernel (VQPC_CHOL_S, default 4)."""
-    return max(1, min(4, int(os.environ.get("VQPC_CHOL_S", "4"))))
+    """Right-hand sides per factor pass of the 2-D cholesky kernel (VQPC_CHOL_S, default 8)."""
+    return max(1, min(8, int(os.environ.get("VQPC_CHOL_S", "8"))))
 
 
 def dgemm_peak(dev, n=8192, reps=3):

@@ -34,7 +34,10 @@ constexpr int PC_T = 256;     // threads per CTA
 constexpr int PC_BS = 32;     // rows per block of the triangular solves
 constexpr int PC_RING = 1024; // y / w ring (rows)
 constexpr int PC_NV = 11;     // per sample slot: D, cS, cW, cE, cN, b, x, r, p, Ap, z
-constexpr int PC_MAXS = 4;
+constexpr int PC_MAXS = 8;
+// y / w ring rows for S slots: 1024 up to S = 4; 512 beyond, so that the ring and two
+// stages still fit 227 KB (W <= PC_WIN keeps W + 3 PC_BS <= 512)
+constexpr int pc_ring(int S) { return S > 4 ? 512 : PC_RING; }
 constexpr int PC_WIN = 256;   // columns left of a block the products cover (>= the envelope width W)
 // per block of a centroid's Linv array and of a stage (doubles): Linv_B [1024] |
 // block metadata [32: first[32], offset of row i's column 0 in the staged rows[32]];
@@ -241,7 +244,8 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
   const CholLayout lay = prm.lay;
   const int n = lay.n, t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int stage_len = PC_LIB + prm.cap;
-  double* ring = dsm + 2 * stage_len;  // [S][PC_RING]
+  constexpr int RING = pc_ring(S);
+  double* ring = dsm + 2 * stage_len;  // [S][RING]
   const unsigned bar0 = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[0]));
   if (t == 0) {
     pc_mbar_init(bar0);
@@ -337,7 +341,7 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
       double* sp = dsm + stg * stage_len;
       const unsigned bar = bar0 + 8u * stg;
       const int e = blk - WB;  // backward: y block entering the window (not left in the ring by the forward sweep)
-      const bool zin = !fwd && e >= 0 && e < lay.nblk - PC_RING / PC_BS;
+      const bool zin = !fwd && e >= 0 && e < lay.nblk - RING / PC_BS;
       if (lane == 0) pc_mbar_expect(bar, PC_LIB * 8u + cbytes + (zin ? S * 256u : 0u));
       __syncwarp();
       auto sa = [](const void* q) { return static_cast<unsigned>(__cvta_generic_to_shared(q)); };
@@ -347,7 +351,7 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
         pc_bulk_g2s(sa(sp), Lip + static_cast<size_t>(blk) * PC_LIB, PC_LIB * 8u, bar);
       } else if (zin && lane >= 8 && lane < 8 + S) {
         const int s = lane - 8;
-        pc_bulk_g2s(sa(ring + s * PC_RING + ((e * PC_BS) & (PC_RING - 1))), vec(s, VZ) + e * PC_BS, 256u, bar);
+        pc_bulk_g2s(sa(ring + s * RING + ((e * PC_BS) & (RING - 1))), vec(s, VZ) + e * PC_BS, 256u, bar);
       }
     };
     auto blk_of = [&](int v) { return v < lay.nblk ? v : nvis - 1 - v; };
@@ -406,7 +410,7 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
               const int j = jw + 4 * ks + ka;
-              const double b = (ra < S && j >= 0) ? ring[ra * PC_RING + (j & (PC_RING - 1))] : 0.0;
+              const double b = (ra < S && j >= 0) ? ring[ra * RING + (j & (RING - 1))] : 0.0;
 #pragma unroll
               for (int mt = 0; mt < 4; ++mt) {
                 const double a = j >= fr[mt] ? dsm[of[mt] + j] : 0.0;
@@ -430,19 +434,26 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
             }
           }
           __syncthreads();
-          const int i = t >> 3, q = t & 7;
+          if (warp < 4) {
+            // y_B = Linv_B T on DMMA: warp = m-tile (8 rows), K = the 32 block columns,
+            // N = the S slots (zero-padded to 8)
+            const int ra = lane >> 2, ka = lane & 3, i = 8 * warp + ra;
+            double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-          for (int s = 0; s < S; ++s) {
-            double y = 0.0;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) y = fma(Li[i * PC_BS + 4 * q + c], tv[s][4 * q + c], y);
-            y += shfl_xor(y, 1);
-            y += shfl_xor(y, 2);
-            y += shfl_xor(y, 4);
-            if (q == 0 && r0 + i < r1) {
-              ring[s * PC_RING + ((r0 + i) & (PC_RING - 1))] = y;
-              vec(s, VZ)[r0 + i] = y;
+            for (int ks = 0; ks < 8; ++ks) {
+              const int k = 4 * ks + ka;
+              pc_dmma(c0, c1, Li[i * PC_BS + k], ra < S ? tv[ra][k] : 0.0);
             }
+            if (r0 + i < r1) {
+              if (2 * ka < S) ring[(2 * ka) * RING + ((r0 + i) & (RING - 1))] = c0;
+              if (2 * ka + 1 < S) ring[(2 * ka + 1) * RING + ((r0 + i) & (RING - 1))] = c1;
+            }
+          }
+          __syncthreads();
+          {
+            // y to HBM, one row x slot per thread (the backward sweep re-reads it by TMA)
+            const int i = t >> 3, q = t & 7;
+            if (q < S && r0 + i < r1) vec(q, VZ)[r0 + i] = ring[q * RING + ((r0 + i) & (RING - 1))];
           }
           // y goes back to HBM; the backward sweep re-reads blocks of it by TMA, the
           // first of them WB + 1 visits after the sweep turns (fence below)
@@ -450,26 +461,31 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
           P2_TOC(3, t_fwd);
         } else {
           if (v == lay.nblk) asm volatile("fence.proxy.async;" ::: "memory");  // this thread's y stores
-          const int c = t >> 3, q = t & 7;
+          if (warp < 4) {
+            // z_B = Linv_B^T w_B on DMMA: warp = m-tile (8 columns c), K = the 32 block
+            // rows, N = the S slots (zero-padded to 8)
+            const int ra = lane >> 2, ka = lane & 3, c = 8 * warp + ra;
+            double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-          for (int s = 0; s < S; ++s) {
-            double z = 0.0;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int i = 4 * q + e;
-              const double w = r0 + i < r1 ? ring[s * PC_RING + ((r0 + i) & (PC_RING - 1))] : 0.0;
-              z = fma(Li[i * PC_BS + c], w, z);
+            for (int ks = 0; ks < 8; ++ks) {
+              const int i = 4 * ks + ka;
+              const double w = ra < S && r0 + i < r1 ? ring[ra * RING + ((r0 + i) & (RING - 1))] : 0.0;
+              pc_dmma(c0, c1, Li[i * PC_BS + c], w);
             }
-            z += shfl_xor(z, 1);
-            z += shfl_xor(z, 2);
-            z += shfl_xor(z, 4);
-            if (q == 0) {
-              tv[s][c] = r0 + c < r1 ? z : 0.0;
-              if (r0 + c < r1) vec(s, VZ)[r0 + c] = z;
-            }
-            if (q == s && r0 + c < r1) rzp[s] = fma(rv, z, rzp[s]);
+            if (2 * ka < S) tv[2 * ka][c] = r0 + c < r1 ? c0 : 0.0;
+            if (2 * ka + 1 < S) tv[2 * ka + 1][c] = r0 + c < r1 ? c1 : 0.0;
           }
           __syncthreads();
+          {
+            const int c = t >> 3, q = t & 7;
+            if (q < S && r0 + c < r1) {
+              const double z = tv[q][c];
+              vec(q, VZ)[r0 + c] = z;
+#pragma unroll
+              for (int s = 0; s < S; ++s)
+                if (q == s) rzp[s] = fma(rv, z, rzp[s]);
+            }
+          }
           const int lo = r0 - lay.W > 0 ? r0 - lay.W : 0;
           {
             // w_j -= sum_i L(r0 + i, j) z_i for the PC_WIN columns left of the block, as
@@ -496,8 +512,8 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
                 pc_dmma(c0, c1, a, bz[ks]);
               }
               if (j >= lo) {
-                if (2 * ka < S) ring[(2 * ka) * PC_RING + (j & (PC_RING - 1))] -= c0;
-                if (2 * ka + 1 < S) ring[(2 * ka + 1) * PC_RING + (j & (PC_RING - 1))] -= c1;
+                if (2 * ka < S) ring[(2 * ka) * RING + (j & (RING - 1))] -= c0;
+                if (2 * ka + 1 < S) ring[(2 * ka + 1) * RING + (j & (RING - 1))] -= c1;
               }
             }
           }

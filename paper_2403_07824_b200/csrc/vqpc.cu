@@ -115,7 +115,7 @@ struct vqpc_ctx {
   DBuf<double> ch_L, ch_Linv, ch_work;
   int64_t ch_ldL = 0, ch_ldLi = 0, ch_nnz = 0;
   int ch_cap = 0;
-  int ch_S = 4;
+  int ch_S = 8;
   cudaStream_t aux = nullptr;              // chunks beyond the solve subset (overlap with the PCG)
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   DBuf<int> aflag;     // assign_mma candidate-list overflow flag
@@ -383,7 +383,7 @@ void run_schedule(vqpc_ctx* c, const double* d_xi, int64_t ld, const int32_t* d_
 }
 
 size_t pchol_smem(const vqpc_ctx* c, int S) {
-  return sizeof(double) * (2 * (static_cast<size_t>(c->ch_cap) + PC_LIB) + static_cast<size_t>(S) * PC_RING);
+  return sizeof(double) * (2 * (static_cast<size_t>(c->ch_cap) + PC_LIB) + static_cast<size_t>(S) * pc_ring(S));
 }
 
 // 2-D `cholesky` kind: label-major order (stable over the cost-ordered queue), work
@@ -404,10 +404,10 @@ void run_pcgchol2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_
     chol_groups_kernel<<<1, 1, 0, c->stream>>>(c->ch_off.p, P, S, c->ch_groups.p, c->ch_ngroups.p);
     launch_check(c);
   }
-  void (*kern)(const PcholParams) = S == 1   ? pcgchol2d_kernel<1>
-                                    : S == 2 ? pcgchol2d_kernel<2>
-                                    : S == 3 ? pcgchol2d_kernel<3>
-                                             : pcgchol2d_kernel<4>;
+  void (*const kerns[PC_MAXS])(const PcholParams) = {
+      pcgchol2d_kernel<1>, pcgchol2d_kernel<2>, pcgchol2d_kernel<3>, pcgchol2d_kernel<4>,
+      pcgchol2d_kernel<5>, pcgchol2d_kernel<6>, pcgchol2d_kernel<7>, pcgchol2d_kernel<8>};
+  void (*kern)(const PcholParams) = kerns[S - 1];
   const size_t smem = pchol_smem(c, S);
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
@@ -815,7 +815,7 @@ void setup_chol2d(vqpc_ctx* c) {
   h2d(c, c->ch_a0.p, a0s.data(), nblk);
   h2d(c, c->ch_bytes.p, bytes.data(), nblk);
   h2d(c, c->ch_bmeta.p, bmeta.data(), bmeta.size());
-  if (W > PC_WIN || W + 3 * PC_BS > PC_RING) throw ApiError{VQPC_INVALID_CONFIG, "cholesky envelope wider than the solve ring"};
+  if (W > PC_WIN || W + 3 * PC_BS > pc_ring(PC_MAXS)) throw ApiError{VQPC_INVALID_CONFIG, "cholesky envelope wider than the solve ring"};
   c->ch_cperm.ensure(n);
   c->ch_first.ensure(n);
   c->ch_start.ensure(n + 1);

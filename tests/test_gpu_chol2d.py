@@ -41,7 +41,7 @@ def test_chol2d_factor_and_apply_bit_identical(r):
     ctx.close()
 
 
-@pytest.mark.parametrize("S", [1, 2, 4])
+@pytest.mark.parametrize("S", [1, 2, 4, 8])
 @pytest.mark.parametrize("r,n_real", [(32, 48), (30, 24)])
 def test_chol2d_solve_parity(monkeypatch, S, r, n_real):
     monkeypatch.setenv("VQPC_CHOL_S", str(S))

@@ -26,6 +26,6 @@ t2 = time.perf_counter()
 res = ctx.run_campaign(xi, cfg["eps"], max_iter=MAXIT)
 t3 = time.perf_counter()
 prof = ctx.profile_read()
-print(f"S={os.environ.get('VQPC_CHOL_S', '4')} context+factor {t1 - t0:.2f} s; campaign {B} samples {t3 - t2:.2f} s "
+print(f"S={os.environ.get('VQPC_CHOL_S', '8')} context+factor {t1 - t0:.2f} s; campaign {B} samples {t3 - t2:.2f} s "
       f"-> {B / (t3 - t2):.1f} samples/s, mean J {res['iterations'].mean():.2f}, status {np.bincount(res['status'])}; "
       f"prof {prof}")
