@@ -35,6 +35,8 @@ constexpr int PC_BS = 32;     // rows per block of the triangular solves
 constexpr int PC_RING = 1024; // y / w ring (rows)
 constexpr int PC_NV = 11;     // per sample slot: D, cS, cW, cE, cN, b, x, r, p, Ap, z
 constexpr int PC_MAXS = 8;
+constexpr int PC_U = 4;   // rows per thread per batch of the elementwise vector passes
+constexpr int PC_U2 = 2;  // ... and of the stencil passes (Ap, b - Ax)
 // y / w ring rows for S slots: 1024 up to S = 4; 512 beyond, so that the ring and two
 // stages still fit 227 KB (W <= PC_WIN keeps W + 3 PC_BS <= 512)
 constexpr int pc_ring(int S) { return S > 4 ? 512 : PC_RING; }
@@ -559,7 +561,22 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
         if (!act[s]) continue;
         double* P = vec(s, VP);
         const double* Z = vec(s, VZ);
-        for (int k = t; k < n; k += PC_T) P[k] = j == 1 ? Z[k] : __dadd_rn(Z[k], __dmul_rn(beta[s], P[k]));
+        // the vector passes batch PC_U rows per thread (loads first, then the same
+        // per-row operations and accumulation order): 8 warps per SM need the MLP
+        for (int k0 = t; k0 < n; k0 += PC_U * PC_T) {
+          double zv[PC_U], pv[PC_U];
+#pragma unroll
+          for (int u = 0; u < PC_U; ++u) {
+            const int k = k0 + u * PC_T;
+            zv[u] = k < n ? Z[k] : 0.0;
+            pv[u] = k < n && j != 1 ? P[k] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < PC_U; ++u) {
+            const int k = k0 + u * PC_T;
+            if (k < n) P[k] = j == 1 ? zv[u] : __dadd_rn(zv[u], __dmul_rn(beta[s], pv[u]));
+          }
+        }
       }
       __syncthreads();
       // Ap and p.Ap (CSR column order S, W, diag, E, N; no contraction)
@@ -569,13 +586,28 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
         if (!act[s]) continue;
         const double* P = vec(s, VP);
         double* AP = vec(s, VAP);
-        for (int k = t; k < n; k += PC_T) {
-          const int4 nb = lay.nbr[k];
-          const double ap = row_apply(vec(s, VS)[k], vec(s, VW)[k], vec(s, VD)[k], vec(s, VE)[k], vec(s, VN)[k],
-                                      nb.x >= 0 ? P[nb.x] : 0.0, nb.y >= 0 ? P[nb.y] : 0.0, P[k],
-                                      nb.z >= 0 ? P[nb.z] : 0.0, nb.w >= 0 ? P[nb.w] : 0.0);
-          AP[k] = ap;
-          part[s] = fma(P[k], ap, part[s]);
+        for (int k0 = t; k0 < n; k0 += PC_U2 * PC_T) {
+          double ap[PC_U2], pk[PC_U2];
+#pragma unroll
+          for (int u = 0; u < PC_U2; ++u) {
+            const int k = k0 + u * PC_T;
+            ap[u] = pk[u] = 0.0;
+            if (k < n) {
+              const int4 nb = lay.nbr[k];
+              pk[u] = P[k];
+              ap[u] = row_apply(vec(s, VS)[k], vec(s, VW)[k], vec(s, VD)[k], vec(s, VE)[k], vec(s, VN)[k],
+                                nb.x >= 0 ? P[nb.x] : 0.0, nb.y >= 0 ? P[nb.y] : 0.0, pk[u],
+                                nb.z >= 0 ? P[nb.z] : 0.0, nb.w >= 0 ? P[nb.w] : 0.0);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < PC_U2; ++u) {
+            const int k = k0 + u * PC_T;
+            if (k < n) {
+              AP[k] = ap[u];
+              part[s] = fma(pk[u], ap[u], part[s]);
+            }
+          }
         }
       }
       pc_block_sums<S>(part, red, warp, lane);
@@ -592,9 +624,25 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
         double* R = vec(s, VR);
         const double* P = vec(s, VP);
         const double* AP = vec(s, VAP);
-        for (int k = t; k < n; k += PC_T) {
-          X[k] = __dadd_rn(X[k], __dmul_rn(alpha[s], P[k]));
-          R[k] = __dsub_rn(R[k], __dmul_rn(alpha[s], AP[k]));
+        for (int k0 = t; k0 < n; k0 += PC_U * PC_T) {
+          double xv[PC_U], pv[PC_U], rv2[PC_U], av[PC_U];
+#pragma unroll
+          for (int u = 0; u < PC_U; ++u) {
+            const int k = k0 + u * PC_T;
+            const bool in = k < n;
+            xv[u] = in ? X[k] : 0.0;
+            pv[u] = in ? P[k] : 0.0;
+            rv2[u] = in ? R[k] : 0.0;
+            av[u] = in ? AP[k] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < PC_U; ++u) {
+            const int k = k0 + u * PC_T;
+            if (k < n) {
+              X[k] = __dadd_rn(xv[u], __dmul_rn(alpha[s], pv[u]));
+              R[k] = __dsub_rn(rv2[u], __dmul_rn(alpha[s], av[u]));
+            }
+          }
         }
       }
       __syncthreads();
@@ -604,13 +652,23 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
         part[s] = 0.0;
         if (!act[s]) continue;
         const double* X = vec(s, VX);
-        for (int k = t; k < n; k += PC_T) {
-          const int4 nb = lay.nbr[k];
-          const double ax = row_apply(vec(s, VS)[k], vec(s, VW)[k], vec(s, VD)[k], vec(s, VE)[k], vec(s, VN)[k],
-                                      nb.x >= 0 ? X[nb.x] : 0.0, nb.y >= 0 ? X[nb.y] : 0.0, X[k],
-                                      nb.z >= 0 ? X[nb.z] : 0.0, nb.w >= 0 ? X[nb.w] : 0.0);
-          const double rt = __dsub_rn(vec(s, VB)[k], ax);
-          part[s] = fma(rt, rt, part[s]);
+        for (int k0 = t; k0 < n; k0 += PC_U2 * PC_T) {
+          double rt[PC_U2];
+#pragma unroll
+          for (int u = 0; u < PC_U2; ++u) {
+            const int k = k0 + u * PC_T;
+            rt[u] = 0.0;
+            if (k < n) {
+              const int4 nb = lay.nbr[k];
+              const double ax = row_apply(vec(s, VS)[k], vec(s, VW)[k], vec(s, VD)[k], vec(s, VE)[k], vec(s, VN)[k],
+                                          nb.x >= 0 ? X[nb.x] : 0.0, nb.y >= 0 ? X[nb.y] : 0.0, X[k],
+                                          nb.z >= 0 ? X[nb.z] : 0.0, nb.w >= 0 ? X[nb.w] : 0.0);
+              rt[u] = __dsub_rn(vec(s, VB)[k], ax);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < PC_U2; ++u)
+            if (k0 + u * PC_T < n) part[s] = fma(rt[u], rt[u], part[s]);
         }
       }
       pc_block_sums<S>(part, red, warp, lane);
