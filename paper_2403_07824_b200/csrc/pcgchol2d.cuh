@@ -35,8 +35,14 @@ constexpr int PC_BS = 32;     // rows per block of the triangular solves
 constexpr int PC_RING = 1024; // y / w ring (rows)
 constexpr int PC_NV = 11;     // per sample slot: D, cS, cW, cE, cN, b, x, r, p, Ap, z
 constexpr int PC_MAXS = 8;
-constexpr int PC_U = 4;   // rows per thread per batch of the elementwise vector passes
-constexpr int PC_U2 = 2;  // ... and of the stencil passes (Ap, b - Ax)
+#ifndef VQPC_PC_U
+#define VQPC_PC_U 4
+#endif
+#ifndef VQPC_PC_U2
+#define VQPC_PC_U2 2
+#endif
+constexpr int PC_U = VQPC_PC_U;    // rows per thread per batch of the elementwise vector passes
+constexpr int PC_U2 = VQPC_PC_U2;  // ... and of the stencil passes (Ap, b - Ax)
 // y / w ring rows for S slots: 1024 up to S = 4; 512 beyond, so that the ring and two
 // stages still fit 227 KB (W <= PC_WIN keeps W + 3 PC_BS <= 512)
 constexpr int pc_ring(int S) { return S > 4 ? 512 : PC_RING; }
