@@ -33,7 +33,7 @@ namespace vqpc {
 constexpr int PC_T = 256;     // threads per CTA
 constexpr int PC_BS = 32;     // rows per block of the triangular solves
 constexpr int PC_RING = 1024; // y / w ring (rows)
-constexpr int PC_NV = 11;     // per sample slot: D, cS, cW, cE, cN, b, x, r, p, Ap, z
+constexpr int PC_NV = 12;     // per sample slot: D, cS, cW, cE, cN, b, x, r, p, Ap, z, x'
 constexpr int PC_MAXS = 8;
 #ifndef VQPC_PC_U
 #define VQPC_PC_U 4
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
   const int ldv = prm.ldv;  // vector stride: n rounded up to whole 32-row blocks (TMA-aligned)
   double* base = prm.work + static_cast<size_t>(blockIdx.x) * S * PC_NV * ldv;
   auto vec = [&](int s, int v) { return base + (static_cast<size_t>(s) * PC_NV + v) * ldv; };
-  enum { VD = 0, VS, VW, VE, VN, VB, VX, VR, VP, VAP, VZ };
+  enum { VD = 0, VS, VW, VE, VN, VB, VX, VR, VP, VAP, VZ, VX2 };
   int64_t vg = 0;  // staged-block visits issued by this CTA (mbarrier phases)
   const int nvis = 2 * lay.nblk;
 
@@ -626,38 +626,22 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
           continue;
         }
         alpha[s] = rz[s] / part[s];
-        double* X = vec(s, VX);
-        double* R = vec(s, VR);
-        const double* P = vec(s, VP);
-        const double* AP = vec(s, VAP);
-        for (int k0 = t; k0 < n; k0 += PC_U * PC_T) {
-          double xv[PC_U], pv[PC_U], rv2[PC_U], av[PC_U];
-#pragma unroll
-          for (int u = 0; u < PC_U; ++u) {
-            const int k = k0 + u * PC_T;
-            const bool in = k < n;
-            xv[u] = in ? X[k] : 0.0;
-            pv[u] = in ? P[k] : 0.0;
-            rv2[u] = in ? R[k] : 0.0;
-            av[u] = in ? AP[k] : 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < PC_U; ++u) {
-            const int k = k0 + u * PC_T;
-            if (k < n) {
-              X[k] = __dadd_rn(xv[u], __dmul_rn(alpha[s], pv[u]));
-              R[k] = __dsub_rn(rv2[u], __dmul_rn(alpha[s], av[u]));
-            }
-          }
-        }
       }
-      __syncthreads();
-      // true residual b - A x (solver.cpp:220-222)
+      // x, r updates fused with the true residual b - A x (solver.cpp:220-222): x_new at
+      // the stencil's points is recomputed from the old x and p with the same two
+      // operations and stored into the other x buffer (iteration j writes buffer j & 1),
+      // so no barrier separates the update from the residual sweep
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         part[s] = 0.0;
         if (!act[s]) continue;
-        const double* X = vec(s, VX);
+        const double a = alpha[s];
+        const double* Xo = vec(s, (j & 1) ? VX : VX2);
+        double* Xn = vec(s, (j & 1) ? VX2 : VX);
+        double* R = vec(s, VR);
+        const double* P = vec(s, VP);
+        const double* AP = vec(s, VAP);
+        auto xnew = [&](int i) { return __dadd_rn(Xo[i], __dmul_rn(a, P[i])); };
         for (int k0 = t; k0 < n; k0 += PC_U2 * PC_T) {
           double rt[PC_U2];
 #pragma unroll
@@ -666,10 +650,13 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
             rt[u] = 0.0;
             if (k < n) {
               const int4 nb = lay.nbr[k];
+              const double xk = xnew(k);
               const double ax = row_apply(vec(s, VS)[k], vec(s, VW)[k], vec(s, VD)[k], vec(s, VE)[k], vec(s, VN)[k],
-                                          nb.x >= 0 ? X[nb.x] : 0.0, nb.y >= 0 ? X[nb.y] : 0.0, X[k],
-                                          nb.z >= 0 ? X[nb.z] : 0.0, nb.w >= 0 ? X[nb.w] : 0.0);
+                                          nb.x >= 0 ? xnew(nb.x) : 0.0, nb.y >= 0 ? xnew(nb.y) : 0.0, xk,
+                                          nb.z >= 0 ? xnew(nb.z) : 0.0, nb.w >= 0 ? xnew(nb.w) : 0.0);
               rt[u] = __dsub_rn(vec(s, VB)[k], ax);
+              Xn[k] = xk;
+              R[k] = __dsub_rn(R[k], __dmul_rn(a, AP[k]));
             }
           }
 #pragma unroll
@@ -719,7 +706,7 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
       const bool solved = st[s] == VQPC_S_CONVERGED || st[s] == VQPC_S_MAX_ITER || st[s] == VQPC_S_BREAKDOWN;
       if (prm.x_out && solved) {
         double* xo = prm.x_out + static_cast<size_t>(gsv[s]) * n;
-        const double* X = vec(s, VX);
+        const double* X = vec(s, (J[s] & 1) ? VX2 : VX);  // iteration J wrote buffer J & 1
         for (int k = t; k < n; k += PC_T) xo[lay.cperm[k]] = J[s] > 0 ? X[k] : 0.0;
       }
     }
