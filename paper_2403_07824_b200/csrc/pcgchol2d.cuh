@@ -452,16 +452,18 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
               const int k = 4 * ks + ka;
               pc_dmma(c0, c1, Li[i * PC_BS + k], ra < S ? tv[ra][k] : 0.0);
             }
+            // y into the ring and to HBM straight from the fragments (the backward sweep
+            // re-reads HBM blocks by TMA); 8 consecutive rows per slot per warp store
             if (r0 + i < r1) {
-              if (2 * ka < S) ring[(2 * ka) * RING + ((r0 + i) & (RING - 1))] = c0;
-              if (2 * ka + 1 < S) ring[(2 * ka + 1) * RING + ((r0 + i) & (RING - 1))] = c1;
+              if (2 * ka < S) {
+                ring[(2 * ka) * RING + ((r0 + i) & (RING - 1))] = c0;
+                vec(2 * ka, VZ)[r0 + i] = c0;
+              }
+              if (2 * ka + 1 < S) {
+                ring[(2 * ka + 1) * RING + ((r0 + i) & (RING - 1))] = c1;
+                vec(2 * ka + 1, VZ)[r0 + i] = c1;
+              }
             }
-          }
-          __syncthreads();
-          {
-            // y to HBM, one row x slot per thread (the backward sweep re-reads it by TMA)
-            const int i = t >> 3, q = t & 7;
-            if (q < S && r0 + i < r1) vec(q, VZ)[r0 + i] = ring[q * RING + ((r0 + i) & (RING - 1))];
           }
           // y goes back to HBM; the backward sweep re-reads blocks of it by TMA, the
           // first of them WB + 1 visits after the sweep turns (fence below)
