@@ -28,30 +28,54 @@
 namespace vqp::gpu {
 
 // What the reference's CampaignConfig cannot express (it is 2-D only and has
-// no IC(0)): the model dimension/size, the preconditioner kind on the GPU, the
-// chunking and the solve subset (BASELINE C5).
+// no IC(0)): the model dimension/size, an optional override of the
+// preconditioner kind, the chunking and the solve subset (BASELINE C5).
 struct GpuOptions {
   int dim = 2;          // 1: N-element 1-D model (size = N); 2: r x r mesh (size = r)
   int size = 0;         // 0: take artifacts.mesh.resolution
-  int precond = VQPC_PC_IC0;
+  int precond = -1;     // -1: CampaignConfig::precond (gpu_precond); else a vqpc_precond (e.g. VQPC_PC_IC0)
   int64_t chunk = 0;
   int64_t solve_limit = -1;
   bool exact_reductions = false;
   int device = 0;
 };
 
+// vqp::Error whose code() is the reference's stable code string (error.hpp:8-19)
+// and whose what() adds the library's detail message (vqpc_last_error).
+class Error : public vqp::Error {
+ public:
+  Error(const char* code, std::string detail) : vqp::Error(code), what_(std::move(detail)) {}
+  const char* what() const noexcept override { return what_.c_str(); }
+
+ private:
+  std::string what_;
+};
+
 inline void check(int code, const vqpc_ctx* ctx = nullptr) {
   if (code == VQPC_OK) return;
-  // same stable code strings as vqp::Error (error.hpp); the message adds detail
   std::string msg = vqpc_error_string(code);
   if (ctx && *vqpc_last_error(ctx)) msg = msg + ": " + vqpc_last_error(ctx);
-  throw vqp::Error(vqpc_error_string(code));
+  throw Error(vqpc_error_string(code), msg);
+}
+
+// CampaignConfig::precond (driver.hpp:13,36) -> the GPU kind that implements it, as
+// build_preconditioner chooses the reference's (driver.cpp:117-126). Kinds without a
+// GPU implementation raise invalid-config instead of silently substituting another.
+inline int gpu_precond(PrecondKind kind) {
+  switch (kind) {
+    case PrecondKind::Cholesky: return VQPC_PC_CHOLESKY;
+    case PrecondKind::Amg: return VQPC_PC_AMG;
+    default:
+      throw Error("invalid-config", std::string("invalid-config: preconditioner kind '") +
+                                        (kind == PrecondKind::Identity ? "identity" : "block_jacobi") +
+                                        "' has no GPU implementation (cholesky, amg; ic0 via GpuOptions::precond)");
+  }
 }
 
 // Device-resident basis + codebook + the P centroid factors. Owns a vqpc_ctx.
 class Context {
  public:
-  Context(const CampaignArtifacts& art, const GpuOptions& opt) {
+  Context(const CampaignArtifacts& art, const GpuOptions& opt, int precond) {
     const Codebook& cb = art.codebook;
     const KLBasis& basis = art.basis;
     vqpc_problem pb{};
@@ -68,7 +92,7 @@ class Context {
     pb.lambdas = cb.t2.lambdas.data();
     pb.centroids = cb.centroids.data();
     pb.latent = cb.latent_centroids.empty() ? nullptr : cb.latent_centroids.data();
-    pb.precond = opt.precond;
+    pb.precond = precond;
     pb.device = opt.device;
     vqpc_ctx* c = nullptr;
     check(vqpc_ctx_create(&pb, &c));
@@ -116,7 +140,7 @@ inline std::vector<int> assign_all(const Context& c, const SampleSet& xi) {
 namespace detail {
 inline SimulationReport campaign(const CampaignConfig& config, const CampaignArtifacts& artifacts,
                                  const SampleSet& realizations, const GpuOptions& opt, std::vector<double>* x) {
-  Context c(artifacts, opt);
+  Context c(artifacts, opt, opt.precond >= 0 ? opt.precond : gpu_precond(config.precond));
   const int64_t B = realizations.n;
   const int P = artifacts.codebook.P;
   std::vector<int32_t> labels(B), iters(B);

@@ -73,7 +73,10 @@ enum vqpc_sample_status {
 
 enum vqpc_method { VQPC_KMEANS = 0, VQPC_CLVQ = 1, VQPC_GRID = 2, VQPC_SIGN_GRID = 3 };
 enum vqpc_map { VQPC_SCALE = 0, VQPC_CDF = 1 };
-enum vqpc_precond { VQPC_PC_IDENTITY = 0, VQPC_PC_CHOLESKY = 1, VQPC_PC_IC0 = 4 };
+/* preconditioner kinds: the reference's PrecondKind (driver.hpp:13) numbering where
+ * one exists (cholesky, amg); IC(0) is new. IDENTITY and block
+ * Jacobi have no GPU implementation (invalid-config). */
+enum vqpc_precond { VQPC_PC_IDENTITY = 0, VQPC_PC_CHOLESKY = 1, VQPC_PC_AMG = 3, VQPC_PC_IC0 = 4 };
 
 /* Everything a campaign needs besides its xi draws (CampaignArtifacts,
  * driver.hpp:77-81, plus the CampaignConfig fields the solve uses). */

@@ -81,9 +81,14 @@ def scaled(cfg, n_realizations=None, ns=None, **kw):
     return c
 
 
+# version of the basis construction rules (2: tie-tolerant sign rule, klbasis._sign_index)
+BASIS_RULES = 2
+
+
 def _key(cfg, what):
     if what == "basis":
         sub = {k: cfg[k] for k in ("dim", "mesh_resolution", "sigma2", "ell", "n_kl", "kl_cutoff")}
+        sub["basis_rules"] = BASIS_RULES
     else:
         sub = {k: cfg[k] for k in ("dim", "mesh_resolution", "sigma2", "ell", "n_kl", "kl_cutoff", "m")}
         sub["quantizer"] = cfg["quantizer"]

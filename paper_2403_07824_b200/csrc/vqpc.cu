@@ -872,7 +872,9 @@ void campaign_device(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, double 
   // PCG launch, so their kernels fill the SMs the PCG's work-queue tail leaves idle
   // instead of preceding the solve. They touch only the scratch rows and their own
   // labels/records; the stats kernel waits for them.
-  const bool overlap = merge && nsolve < B && std::getenv("VQPC_NO_OVERLAP") == nullptr;
+  // (not while per-launch events are recorded: profiled steps run serially so that the
+  // kernel times do not overlap)
+  const bool overlap = merge && nsolve < B && !c->prof && std::getenv("VQPC_NO_OVERLAP") == nullptr;
   const int64_t split_c0 = overlap ? std::min<int64_t>(B, ceil_div(nsolve, chunk) * chunk) : B;
   auto realise_assign_only = [&](int64_t c0) {  // a chunk beyond the solve subset
     const int64_t nb = std::min(chunk, B - c0);

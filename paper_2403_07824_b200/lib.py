@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("VQPC_LIB", os.path.join(HERE, "libvqpc.so"))
 
 METHODS = {"kmeans": 0, "clvq": 1, "grid": 2, "sign_grid": 3}
 MAPS = {"scale": 0, "cdf": 1}
-PRECONDS = {"identity": 0, "cholesky": 1, "ic0": 4}
+PRECONDS = {"identity": 0, "cholesky": 1, "amg": 3, "ic0": 4}
 STATUS = {0: "converged", 1: "max_iter", 2: "breakdown", 3: "coefficient-overflow", 4: "invalid-latent",
           5: "invalid-coefficient", 6: "not-solved"}
 

@@ -36,7 +36,28 @@ def test_cpu_sample_size_bounded():
     from paper_2403_07824_b200 import campaign
     b = _bench()
     sizes = {k: b.cpu_sample_size(campaign.CONFIGS[k]) for k in ("C1", "C2", "C3", "C4", "C5")}
-    assert sizes["C4"] <= 64 and sizes["C2"] <= 1024 and all(v >= 16 for v in sizes.values())
+    # (all threads, one thread): C4 >= 32 samples, C2 >= 8192, one-thread legs bounded
+    assert 32 <= sizes["C4"][0] <= 64 and sizes["C4"][1] <= 8
+    assert sizes["C2"][0] >= 8192 and sizes["C2"][1] <= 512
+    assert all(a >= 16 and 1 <= o <= a for a, o in sizes.values())
+
+
+def test_default_workload_is_c4():
+    b = _bench()
+    import sys as _s
+    old = _s.argv
+    _s.argv = ["bench.py"]
+    try:
+        assert b.parse().config == "C4"
+    finally:
+        _s.argv = old
+
+
+def test_c5_value_counts_solved_samples():
+    from paper_2403_07824_b200 import campaign
+    b = _bench()
+    assert b.solved_count(campaign.CONFIGS["C5"], 1 << 20) == 1 << 16
+    assert b.solved_count(campaign.CONFIGS["C2"], 1 << 17) == 1 << 17
 
 
 def _prof(kind, ms, launches=3):
@@ -73,6 +94,9 @@ def test_roofline_pcg1d_and_realise_fp64(monkeypatch):
     roof = b.roofline(cfg5, _prof("realise", 3 * 100.0), 0, 1 << 14, 3, 0)
     assert roof["kernel"] == "realise"
     assert roof["achieved"] == pytest.approx(2.0 * cfg5["mesh_resolution"] * cfg5["n_kl"] * (1 << 14) / 0.1 / 1e12)
+    # the effective mode count (after the cutoff) is what the contraction uses
+    roof = b.roofline(dict(cfg5, _K=39), _prof("realise", 3 * 100.0), 0, 1 << 14, 3, 0)
+    assert roof["achieved"] == pytest.approx(2.0 * cfg5["mesh_resolution"] * 39 * (1 << 14) / 0.1 / 1e12)
 
 
 def test_per_kernel_rooflines():

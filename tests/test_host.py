@@ -22,9 +22,11 @@ def test_kl_basis_1d_properties():  # SPEC acceptance 2 (M-orthonormality, energ
     assert np.all(np.diff(lam) <= 0)
     G = (phi * mass) @ phi.T
     assert np.abs(G - np.eye(lam.size)).max() < 1e-10
-    for k in range(lam.size):  # sign convention (field.cpp:72-79)
-        i = int(np.argmax(np.abs(phi[k])))
+    for k in range(lam.size):  # sign convention (field.cpp:72-79), exact ties to the first index
+        i = klbasis._sign_index(phi[k])
         assert phi[k, i] > 0
+        a = np.abs(phi[k])
+        assert a[i] >= a.max() * (1 - 1e-9) and np.all(a[:i] < a.max() * (1 - 1e-9))
     xi = np.random.default_rng(0).standard_normal((10, lam.size))
     h = (xi * np.sqrt(lam)) @ phi
     e1 = (h * h * mass).sum(1)
@@ -47,6 +49,31 @@ def test_kl_basis_2d_small_matches_dense():
     assert np.allclose(b["eigenvalues"], w[:12], rtol=1e-9)
     G = (b["eigenvectors"] * b["mass"]) @ b["eigenvectors"].T
     assert np.abs(G - np.eye(12)).max() < 1e-9
+
+
+def test_kl_basis_2d_host_independent():
+    """The basis does not depend on the eigensolver's start vector (a stand-in for
+    the host): the corner masses split the lambda_ij / lambda_ji pairs of the
+    separable kernel, so every mode is simple and even or odd under the grid
+    transposition T, and the sign rule's exact ties (odd modes) go to the first
+    index."""
+    r = 20
+    a = klbasis.build_kl_basis_2d(r, 1.0, 0.2, 24, v0_seed=1)
+    b = klbasis.build_kl_basis_2d(r, 1.0, 0.2, 24, v0_seed=2)
+    assert np.allclose(a["eigenvalues"], b["eigenvalues"], rtol=1e-11, atol=0)
+    assert np.abs(a["eigenvectors"] - b["eigenvectors"]).max() < 1e-7
+    lam = a["eigenvalues"]
+    assert np.all(np.diff(lam) < 0)
+    side = r + 1
+    perm = np.arange(side * side).reshape(side, side).T.reshape(-1)
+    for phi in a["eigenvectors"]:
+        assert min(np.abs(phi[perm] - phi).max(), np.abs(phi[perm] + phi).max()) < 1e-6 * np.abs(phi).max()
+
+
+def test_sign_rule_ties_take_first_index():
+    v = np.array([0.1, -0.5, 0.2, 0.5 * (1 + 1e-13), -0.3])
+    assert klbasis._sign_index(v) == 1
+    assert klbasis._sign_index(np.array([0.1, 0.4, -0.5])) == 2
 
 
 def test_artifact_round_trip(tmp_path):
