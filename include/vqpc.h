@@ -132,6 +132,16 @@ int vqpc_centroid_coefficients(vqpc_ctx* ctx, double* kappa_out);
 /* Apply M_p^{-1} to r (n) -> z (n) for one centroid (Preconditioner::apply). */
 int vqpc_precond_apply(vqpc_ctx* ctx, int p, const double* r, double* z);
 
+/* ---- SA-AMG kind (VQPC_PC_AMG, 2-D): the hierarchy of centroid p built by
+ * vqpc_factor_centroids (AmgPreconditioner ctor, amg.cpp:132-197). info[4l..4l+3]
+ * = rows, nnz(A_l), nnz(P_l), columns of P_l; *dense_n = size of the coarsest
+ * dense factor (0: smoother-only bottom). vqpc_amg_level copies level l's CSR
+ * operator, its inverse diagonal, its prolongator (CSR, none on the coarsest) and,
+ * on the coarsest level, the dense lower factor (row-major, nullable). */
+int vqpc_amg_info(const vqpc_ctx* ctx, int p, int max_levels, int64_t* info, int* nlev, int* dense_n);
+int vqpc_amg_level(const vqpc_ctx* ctx, int p, int l, int* a_rp, int* a_col, double* a_val, double* inv_diag,
+                   int* p_rp, int* p_col, double* p_val, double* L);
+
 /* ---- (b) assignment: labels[i] = assign(codebook, xi_i[0:m]) ------------- */
 int vqpc_assign(vqpc_ctx* ctx, const double* xi, int64_t B, int ld, int32_t* labels);
 int vqpc_assign_d(vqpc_ctx* ctx, const double* d_xi, int64_t B, int ld, int32_t* d_labels);

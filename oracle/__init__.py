@@ -29,7 +29,7 @@ ERRORS = {
 }
 METHODS = {"kmeans": 0, "clvq": 1, "grid": 2, "sign_grid": 3}
 MAPS = {"scale": 0, "cdf": 1}
-PRECONDS = {"identity": 0, "cholesky": 1, "ic0": 4}
+PRECONDS = {"identity": 0, "cholesky": 1, "amg": 3, "ic0": 4}
 
 
 class OracleError(RuntimeError):
@@ -225,11 +225,28 @@ class Codebook:
                 _p(self.centroids), _p(self.latent))
 
 
-def assign(cb: Codebook, xi):
+def assign(cb: Codebook, xi, threads=1):
+    """quantizer.cpp:134-145 per row. threads > 1 splits the rows over Python
+    threads (ctypes releases the GIL; rows are independent, so the labels do not
+    depend on the split)."""
     xi = f64(np.atleast_2d(xi))
     B, ld = xi.shape
     labels = np.empty(B, np.int32)
-    _check(lib().vqpo_assign(*cb.args, _p(xi), I64(B), I(ld), _p(labels)))
+    if threads <= 1 or B < 2 * threads:
+        _check(lib().vqpo_assign(*cb.args, _p(xi), I64(B), I(ld), _p(labels)))
+        return labels
+    from concurrent.futures import ThreadPoolExecutor
+    bounds = np.linspace(0, B, threads + 1).astype(np.int64)
+
+    def part(t):
+        a, b = int(bounds[t]), int(bounds[t + 1])
+        sub = xi[a:b]
+        out = np.empty(b - a, np.int32)
+        _check(lib().vqpo_assign(*cb.args, _p(sub), I64(b - a), I(ld), _p(out)))
+        labels[a:b] = out
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(part, range(threads)))
     return labels
 
 
@@ -298,6 +315,31 @@ class PreconditionerSet:
         _check(lib().vqpo_pset_from_coefficients(I(dim), I(size), I(PRECONDS[kind]), I(kappa.shape[0]), _p(kappa),
                                                  C.byref(h)))
         return cls(h, dim, size)
+
+    def amg_levels(self, p):
+        """SA-AMG hierarchy of centroid p: list of dicts (A CSR, inv_diag, P CSR) and
+        the coarsest dense Cholesky factor (amg.cpp:132-197 restated)."""
+        info = np.zeros(4 * 64, np.int64)
+        nlev, dn = I(), I()
+        _check(lib().vqpo_pset_amg_info(self.h, I(p), I(64), _p(info), C.byref(nlev), C.byref(dn)))
+        out = []
+        for l in range(nlev.value):
+            n, nnz, pnnz, nc = (int(v) for v in info[4 * l:4 * l + 4])
+            a_rp, a_col, a_val = np.empty(n + 1, np.int32), np.empty(nnz, np.int32), np.empty(nnz)
+            inv = np.empty(n)
+            p_rp = np.empty(n + 1, np.int32) if pnnz else np.empty(1, np.int32)
+            p_col, p_val = np.empty(max(pnnz, 1), np.int32), np.empty(max(pnnz, 1))
+            last = l + 1 == nlev.value
+            L = np.empty(dn.value * dn.value) if last and dn.value else None
+            _check(lib().vqpo_pset_amg_level(self.h, I(p), I(l), _p(a_rp), _p(a_col), _p(a_val), _p(inv), _p(p_rp),
+                                             _p(p_col), _p(p_val), _p(L) if L is not None else None))
+            lv = dict(n=n, A=(a_rp, a_col, a_val), inv_diag=inv, nc=nc)
+            if pnnz:
+                lv["P"] = (p_rp, p_col[:pnnz], p_val[:pnnz])
+            if L is not None:
+                lv["L"] = L.reshape(dn.value, dn.value)
+            out.append(lv)
+        return out
 
     def __del__(self):
         if getattr(self, "h", None):

@@ -495,6 +495,347 @@ struct IC0Preconditioner final : Preconditioner {
   const char* kind() const override { return "ic0"; }
 };
 
+// ---- SA-AMG (amg.cpp:40-230; the reference's default kind, driver.hpp:36) ----
+// Restated operation for operation where the reference's arithmetic is its own
+// (strength test, aggregation passes, power iteration seed, damping constant),
+// and with Eigen's evaluation orders written out where it delegates to Eigen:
+//  * sparse * dense into a fresh vector: per row, sum from the first product in
+//    ascending column order (col-major scatter, amg.cpp:114, 206, 223);
+//  * `r - A x` assigned to a vector (amg.cpp:219): Eigen rewrites it to
+//    res = r; res -= A x, i.e. per row r_i - a_ij1 x_j1 - a_ij2 x_j2 - ...;
+//  * `x += P c` (amg.cpp:221): x_i += P_ik c_k in ascending k;
+//  * P^T v (amg.cpp:220): per coarse row, sum over the fine rows in ascending order;
+//  * sparse * sparse (amg.cpp:177, 179): Eigen's conservative product, every
+//    result entry the first product then += in ascending inner index, every
+//    touched entry stored (explicit zeros included);
+//  * norms (v.normalize(), w.norm()): serial sums (Eigen vectorises them:
+//    parity with Eigen's bits is unpinned there, as everywhere Eigen computes);
+//  * the coarsest direct solve (Eigen LLT / SimplicialLLT, amg.cpp:186-193):
+//    a dense column Cholesky, left-looking with sequential subtraction in
+//    ascending k, and column-oriented forward (k ascending) / backward (k
+//    descending) substitution — the order the GPU's warp solve reproduces.
+struct AmgOptions {
+  double theta = 0.08;           // strength_threshold (solver.hpp:36)
+  double omega = 2.0 / 3.0;      // jacobi_weight
+  double damping = 4.0 / 3.0;    // prolongator_damping
+  int power_iterations = 10;
+  int coarse_size = 64;
+  int max_levels = 32;
+};
+
+// Transpose of an (n x ncols) CSR: row j lists column j's entries in ascending row order.
+static Csr csr_transpose(const Csr& A, int ncols) {
+  Csr T;
+  T.n = ncols;
+  T.row_ptr.assign(ncols + 1, 0);
+  for (int k = 0; k < A.row_ptr[A.n]; ++k) T.row_ptr[A.col[k] + 1]++;
+  for (int j = 0; j < ncols; ++j) T.row_ptr[j + 1] += T.row_ptr[j];
+  T.col.resize(A.col.size());
+  T.val.resize(A.val.size());
+  std::vector<int> pos(T.row_ptr.begin(), T.row_ptr.end() - 1);
+  for (int i = 0; i < A.n; ++i)
+    for (int k = A.row_ptr[i]; k < A.row_ptr[i + 1]; ++k) {
+      const int p = pos[A.col[k]]++;
+      T.col[p] = i;
+      T.val[p] = A.val[k];
+    }
+  return T;
+}
+
+// Eigen's conservative sparse product C = A B (A: n x m by rows, B: m x q by
+// rows), column-major semantics: C(i, j) = sum over k ascending of A(i, k) B(k, j),
+// the first product assigned. Computed here from B's columns (Bt) and A's
+// columns (At): for column j, for k ascending in B(:, j), for i in A(:, k).
+static Csr spgemm_eigen(const Csr& At, int n, const Csr& Bt) {
+  const int q = Bt.n;
+  std::vector<std::vector<std::pair<int, double>>> cols(q);
+  std::vector<double> vals(n, 0.0);
+  std::vector<char> mask(n, 0);
+  std::vector<int> touched;
+  for (int j = 0; j < q; ++j) {
+    touched.clear();
+    for (int e = Bt.row_ptr[j]; e < Bt.row_ptr[j + 1]; ++e) {
+      const int k = Bt.col[e];
+      const double y = Bt.val[e];
+      for (int f = At.row_ptr[k]; f < At.row_ptr[k + 1]; ++f) {
+        const int i = At.col[f];
+        const double x = At.val[f];
+        if (!mask[i]) {
+          mask[i] = 1;
+          vals[i] = x * y;
+          touched.push_back(i);
+        } else {
+          vals[i] += x * y;
+        }
+      }
+    }
+    std::sort(touched.begin(), touched.end());
+    for (int i : touched) {
+      cols[j].push_back({i, vals[i]});
+      mask[i] = 0;
+    }
+  }
+  // assemble by rows (n x q)
+  Csr C;
+  C.n = n;
+  C.row_ptr.assign(n + 1, 0);
+  for (int j = 0; j < q; ++j)
+    for (auto& e : cols[j]) C.row_ptr[e.first + 1]++;
+  for (int i = 0; i < n; ++i) C.row_ptr[i + 1] += C.row_ptr[i];
+  C.col.resize(C.row_ptr[n]);
+  C.val.resize(C.row_ptr[n]);
+  std::vector<int> pos(C.row_ptr.begin(), C.row_ptr.end() - 1);
+  for (int j = 0; j < q; ++j)
+    for (auto& e : cols[j]) {
+      const int p = pos[e.first]++;
+      C.col[p] = j;
+      C.val[p] = e.second;
+    }
+  return C;
+}
+
+// greedy aggregation over the strength graph (amg.cpp:40-106)
+static std::vector<int> amg_aggregate(const Csr& A, const Csr& At, const std::vector<double>& diag, double theta,
+                                      int& count) {
+  const int n = A.n;
+  std::vector<std::vector<int>> strong(n);
+  for (int i = 0; i < n; ++i)
+    for (int k = A.row_ptr[i]; k < A.row_ptr[i + 1]; ++k) {
+      const int j = A.col[k];
+      if (j == i) continue;
+      if (std::abs(A.val[k]) >= theta * std::sqrt(diag[i] * diag[j])) strong[i].push_back(j);
+    }  // row i's columns ascend, so strong[i] is already sorted (amg.cpp:56)
+  std::vector<int> agg(n, -1);
+  count = 0;
+  for (int i = 0; i < n; ++i) {  // pass 1
+    if (agg[i] >= 0) continue;
+    bool free = true;
+    for (int j : strong[i])
+      if (agg[j] >= 0) {
+        free = false;
+        break;
+      }
+    if (!free) continue;
+    agg[i] = count;
+    for (int j : strong[i]) agg[j] = count;
+    ++count;
+  }
+  const std::vector<int> pass1 = agg;
+  for (int i = 0; i < n; ++i) {  // pass 2: column i of A (InnerIterator over column i)
+    if (agg[i] >= 0) continue;
+    int best = -1;
+    double best_w = -1.0;
+    for (int k = At.row_ptr[i]; k < At.row_ptr[i + 1]; ++k) {
+      const int j = At.col[k];
+      if (j == i || pass1[j] < 0) continue;
+      if (!std::binary_search(strong[i].begin(), strong[i].end(), j)) continue;
+      const double w = std::abs(At.val[k]);
+      if (w > best_w) {
+        best_w = w;
+        best = pass1[j];
+      }
+    }
+    if (best >= 0) agg[i] = best;
+  }
+  for (int i = 0; i < n; ++i) {  // pass 3
+    if (agg[i] >= 0) continue;
+    agg[i] = count;
+    for (int j : strong[i])
+      if (agg[j] < 0) agg[j] = count;
+    ++count;
+  }
+  return agg;
+}
+
+static double amg_spectral_radius(const Csr& A, const std::vector<double>& inv_diag, int iterations) {
+  const int n = A.n;
+  std::vector<double> v(n), w(n);
+  for (int i = 0; i < n; ++i) v[i] = uniform_open01(0x5ca1ab1eu, static_cast<uint64_t>(i), 0) - 0.5;
+  double nrm = 0.0;
+  for (int i = 0; i < n; ++i) nrm += v[i] * v[i];
+  nrm = std::sqrt(nrm);
+  if (nrm > 0.0)
+    for (int i = 0; i < n; ++i) v[i] /= nrm;
+  double rho = 1.0;
+  for (int it = 0; it < iterations; ++it) {
+    A.matvec(v.data(), w.data());
+    for (int i = 0; i < n; ++i) w[i] = inv_diag[i] * w[i];
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += w[i] * w[i];
+    rho = std::sqrt(s);
+    if (!(rho > 0.0)) return 1.0;
+    for (int i = 0; i < n; ++i) v[i] = w[i] / rho;
+  }
+  return rho;
+}
+
+struct AmgLevel {
+  Csr A;                     // this level's operator (by rows)
+  std::vector<double> inv_diag;
+  Csr P, Pt;                 // prolongator (n x nc) by rows, and by columns; empty on the coarsest
+  int nc = 0;
+};
+
+struct AmgPreconditioner final : Preconditioner {
+  AmgOptions opt;
+  std::vector<AmgLevel> levels;
+  int dense_n = 0;           // > 0: dense Cholesky of the coarsest operator
+  std::vector<double> Lc;    // dense_n x dense_n, row-major, lower triangle
+
+  explicit AmgPreconditioner(const Csr& A_in, const AmgOptions& o = {}) : opt(o) {
+    Csr A = A_in;
+    for (int depth = 0;; ++depth) {
+      AmgLevel lv;
+      lv.A = A;
+      const int n = A.n;
+      std::vector<double> diag(n, 0.0);
+      for (int i = 0; i < n; ++i) diag[i] = A.at(i, i);
+      lv.inv_diag.resize(n);
+      for (int i = 0; i < n; ++i) {
+        lv.inv_diag[i] = 1.0 / diag[i];
+        if (!std::isfinite(lv.inv_diag[i])) throw Err(NOT_SPD);
+      }
+      const bool can_coarsen = depth + 1 < opt.max_levels && n > opt.coarse_size;
+      if (!can_coarsen) {
+        levels.push_back(std::move(lv));
+        break;
+      }
+      const Csr At = csr_transpose(A, n);
+      int nc = 0;
+      const std::vector<int> agg = amg_aggregate(A, At, diag, opt.theta, nc);
+      if (nc >= n) {
+        levels.push_back(std::move(lv));
+        break;
+      }
+      std::vector<int> size(nc, 0);
+      for (int i = 0; i < n; ++i) size[agg[i]] += 1;
+      // tentative prolongator T (n x nc), by columns: column c = aggregate c's rows ascending
+      Csr Tt;
+      Tt.n = nc;
+      Tt.row_ptr.assign(nc + 1, 0);
+      for (int i = 0; i < n; ++i) Tt.row_ptr[agg[i] + 1]++;
+      for (int c = 0; c < nc; ++c) Tt.row_ptr[c + 1] += Tt.row_ptr[c];
+      Tt.col.resize(n);
+      Tt.val.resize(n);
+      {
+        std::vector<int> pos(Tt.row_ptr.begin(), Tt.row_ptr.end() - 1);
+        for (int i = 0; i < n; ++i) {
+          const int p = pos[agg[i]]++;
+          Tt.col[p] = i;
+          Tt.val[p] = 1.0 / std::sqrt(static_cast<double>(size[agg[i]]));
+        }
+      }
+      const double rho = amg_spectral_radius(A, lv.inv_diag, opt.power_iterations);
+      // S = I - (damping / rho) (D^{-1} A), the pattern of A plus the diagonal
+      const double c = opt.damping / rho;
+      Csr S;
+      S.n = n;
+      S.row_ptr.assign(n + 1, 0);
+      for (int i = 0; i < n; ++i) {
+        bool has_diag = false;
+        for (int k = A.row_ptr[i]; k < A.row_ptr[i + 1]; ++k) {
+          const int j = A.col[k];
+          if (!has_diag && j > i) {  // identity entry where A stores no diagonal (not on SPD input)
+            S.col.push_back(i);
+            S.val.push_back(1.0);
+            has_diag = true;
+          }
+          const double x = c * (lv.inv_diag[i] * A.val[k]);
+          S.col.push_back(j);
+          S.val.push_back(j == i ? 1.0 - x : 0.0 - x);
+          if (j == i) has_diag = true;
+        }
+        if (!has_diag) {
+          S.col.push_back(i);
+          S.val.push_back(1.0);
+        }
+        S.row_ptr[i + 1] = static_cast<int>(S.col.size());
+      }
+      const Csr St = csr_transpose(S, n);
+      lv.P = spgemm_eigen(St, n, Tt);          // P = S T (n x nc)
+      lv.Pt = csr_transpose(lv.P, nc);
+      lv.nc = nc;
+      // A_c = (P^T A) P: first PtA (nc x n), then (PtA) P
+      const Csr PtA = spgemm_eigen(lv.P, nc, At);    // columns of P^T are P's rows; B = A by columns
+      const Csr PtAt = csr_transpose(PtA, n);
+      Csr Ac = spgemm_eigen(PtAt, nc, lv.Pt);
+      levels.push_back(std::move(lv));
+      A = std::move(Ac);
+    }
+    const AmgLevel& last = levels.back();
+    const int nc = last.A.n;
+    if (nc <= opt.coarse_size || levels.size() > 1) {
+      dense_n = nc;
+      Lc.assign(static_cast<size_t>(nc) * nc, 0.0);
+      for (int j = 0; j < nc; ++j) {
+        double d = last.A.at(j, j);
+        for (int k = 0; k < j; ++k) d -= Lc[j * nc + k] * Lc[j * nc + k];
+        if (!(d > 0.0)) throw Err(NOT_SPD);
+        const double ljj = std::sqrt(d);
+        Lc[j * nc + j] = ljj;
+        for (int i = j + 1; i < nc; ++i) {
+          double s = last.A.at(i, j);
+          for (int k = 0; k < j; ++k) s -= Lc[i * nc + k] * Lc[j * nc + k];
+          Lc[i * nc + j] = s / ljj;
+        }
+      }
+    }
+  }
+
+  void dense_solve(const double* r, double* x) const {
+    const int nc = dense_n;
+    std::vector<double> s(r, r + nc);
+    for (int k = 0; k < nc; ++k) {  // L y = r, column-oriented
+      const double yk = s[k] / Lc[k * nc + k];
+      s[k] = yk;
+      for (int i = k + 1; i < nc; ++i) s[i] -= Lc[i * nc + k] * yk;
+    }
+    for (int k = nc - 1; k >= 0; --k) {  // L^T x = y, column-oriented
+      const double xk = s[k] / Lc[k * nc + k];
+      s[k] = xk;
+      for (int i = 0; i < k; ++i) s[i] -= Lc[k * nc + i] * xk;
+    }
+    std::copy(s.begin(), s.end(), x);
+  }
+
+  // one V-cycle from zero on level l (amg.cpp:210-225)
+  void cycle(size_t l, const double* r, double* x) const {
+    const AmgLevel& lv = levels[l];
+    const int n = lv.A.n;
+    const double w = opt.omega;
+    if (l + 1 == levels.size()) {
+      if (dense_n > 0) {
+        dense_solve(r, x);
+        return;
+      }
+      std::vector<double> t(n);
+      for (int i = 0; i < n; ++i) x[i] = w * (lv.inv_diag[i] * r[i]);
+      lv.A.matvec(x, t.data());
+      for (int i = 0; i < n; ++i) x[i] += w * (lv.inv_diag[i] * (r[i] - t[i]));
+      return;
+    }
+    std::vector<double> res(n), t(n), rc(lv.nc), xc(lv.nc);
+    for (int i = 0; i < n; ++i) x[i] = w * (lv.inv_diag[i] * r[i]);  // pre-smooth from 0
+    for (int i = 0; i < n; ++i) {  // residual = r - A x (Eigen: res = r; res -= A x)
+      double s = r[i];
+      for (int k = lv.A.row_ptr[i]; k < lv.A.row_ptr[i + 1]; ++k) s -= lv.A.val[k] * x[lv.A.col[k]];
+      res[i] = s;
+    }
+    lv.Pt.matvec(res.data(), rc.data());  // P^T residual
+    cycle(l + 1, rc.data(), xc.data());
+    for (int i = 0; i < n; ++i) {  // x += P coarse
+      double s = x[i];
+      for (int k = lv.P.row_ptr[i]; k < lv.P.row_ptr[i + 1]; ++k) s += lv.P.val[k] * xc[lv.P.col[k]];
+      x[i] = s;
+    }
+    lv.A.matvec(x, t.data());  // post-smooth
+    for (int i = 0; i < n; ++i) x[i] += w * (lv.inv_diag[i] * (r[i] - t[i]));
+  }
+
+  void apply(const double* r, double* z) const override { cycle(0, r, z); }
+  const char* kind() const override { return "amg"; }
+};
+
 // ---- pcg: solver.cpp:186-245 -------------------------------------------------
 struct Record {
   int iterations = 0;
@@ -758,7 +1099,7 @@ static std::vector<double> kmeans(const double* samples, int n, int m, const dou
 }
 
 // ---- campaign: driver.cpp:193-281 with the 1-D/2-D model switch ---------------
-enum Precond : int { PC_IDENTITY = 0, PC_CHOLESKY = 1, PC_IC0 = 4 };
+enum Precond : int { PC_IDENTITY = 0, PC_CHOLESKY = 1, PC_AMG = 3, PC_IC0 = 4 };
 
 struct Model {
   int dim = 1;   // 1: N elements; 2: r x r structured mesh
@@ -774,6 +1115,7 @@ static std::unique_ptr<Preconditioner> build_preconditioner(int kind, const Mode
   switch (kind) {
     case PC_IDENTITY: return std::make_unique<IdentityPreconditioner>(A.n);
     case PC_CHOLESKY: return std::make_unique<CholeskyPreconditioner>(A);
+    case PC_AMG: return std::make_unique<AmgPreconditioner>(A);
     case PC_IC0:
       if (model.dim != 2) throw Err(INVALID_CONFIG);
       return std::make_unique<IC0Preconditioner>(A, model.size);
@@ -1023,6 +1365,49 @@ int vqpo_pset_from_coefficients(int dim, int size, int kind, int P, const double
       set->M.back()->built_from = p;
     }
     *out = set.release();
+  })
+}
+
+// SA-AMG hierarchy of centroid p (AmgOptions::level_sizes_out, solver.hpp:42, plus
+// the operators, for bit-level checks of the GPU library's own setup).
+// info[l*4 + 0..3] = n_l, nnz(A_l), nnz(P_l), nc_l; returns the level count in *nlev
+// and the coarsest dense size in *dense_n.
+int vqpo_pset_amg_info(void* h, int p, int max_levels, int64_t* info, int* nlev, int* dense_n) {
+  VQPO_GUARD({
+    auto* set = static_cast<PreconditionerSet*>(h);
+    const auto* amg = dynamic_cast<const AmgPreconditioner*>(set->M.at(p).get());
+    if (!amg) throw Err(INVALID_CONFIG);
+    *nlev = static_cast<int>(amg->levels.size());
+    *dense_n = amg->dense_n;
+    for (int l = 0; l < *nlev && l < max_levels; ++l) {
+      const AmgLevel& lv = amg->levels[l];
+      info[l * 4 + 0] = lv.A.n;
+      info[l * 4 + 1] = lv.A.row_ptr[lv.A.n];
+      info[l * 4 + 2] = lv.P.n ? lv.P.row_ptr[lv.P.n] : 0;
+      info[l * 4 + 3] = lv.nc;
+    }
+  })
+}
+
+// copy level l's A (row_ptr n+1, col, val), inv_diag (n) and P (row_ptr n+1,
+// col, val; empty on the coarsest); L (dense_n^2, row-major) when l is the last level
+int vqpo_pset_amg_level(void* h, int p, int l, int* a_rp, int* a_col, double* a_val, double* inv_diag, int* p_rp,
+                        int* p_col, double* p_val, double* L) {
+  VQPO_GUARD({
+    auto* set = static_cast<PreconditionerSet*>(h);
+    const auto* amg = dynamic_cast<const AmgPreconditioner*>(set->M.at(p).get());
+    if (!amg) throw Err(INVALID_CONFIG);
+    const AmgLevel& lv = amg->levels.at(l);
+    std::copy(lv.A.row_ptr.begin(), lv.A.row_ptr.end(), a_rp);
+    std::copy(lv.A.col.begin(), lv.A.col.end(), a_col);
+    std::copy(lv.A.val.begin(), lv.A.val.end(), a_val);
+    std::copy(lv.inv_diag.begin(), lv.inv_diag.end(), inv_diag);
+    if (lv.P.n) {
+      std::copy(lv.P.row_ptr.begin(), lv.P.row_ptr.end(), p_rp);
+      std::copy(lv.P.col.begin(), lv.P.col.end(), p_col);
+      std::copy(lv.P.val.begin(), lv.P.val.end(), p_val);
+    }
+    if (L && l + 1 == static_cast<int>(amg->levels.size())) std::copy(amg->Lc.begin(), amg->Lc.end(), L);
   })
 }
 

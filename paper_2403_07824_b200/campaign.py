@@ -54,6 +54,10 @@ CONFIGS = {
     # matrix, solver.cpp:72-111) instead of IC(0); SURVEY 8(f)-1
     "C4chol": _cfg(name="C4chol", dim=2, mesh_resolution=256, sigma2=1.0, ell=0.2, n_kl=100, m=10,
                    n_realizations=8192, precond="cholesky", quantizer=dict(P=32, ns=20_000)),
+    # C4amg: C4 with the reference's DEFAULT kind, SA-AMG (PrecondKind::Amg, driver.hpp:36;
+    # amg.cpp:40-230, one V-cycle per PCG iteration); SURVEY 8(f)-3
+    "C4amg": _cfg(name="C4amg", dim=2, mesh_resolution=256, sigma2=1.0, ell=0.2, n_kl=100, m=10,
+                  n_realizations=8192, precond="amg", quantizer=dict(P=32, ns=20_000)),
     # C5: realisation + assignment stress test; PCG on a 2^16 subset; no KL cutoff
     "C5": _cfg(name="C5", dim=1, mesh_resolution=8192, sigma2=1.0, ell=0.1, n_kl=256, m=64, n_realizations=1 << 20,
                kl_cutoff=False, chunk=1 << 14, solve_subset=1 << 16, quantizer=dict(P=4096, ns=1 << 18)),

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cstdint>
 #include <cmath>
@@ -17,6 +18,9 @@
 #include <string>
 #include <vector>
 
+#include <thread>
+
+#include "amg_setup.cuh"
 #include "assign.cuh"
 #include "assign_mma.cuh"
 #include "bucket.cuh"
@@ -25,6 +29,7 @@
 #include "pcg1d.cuh"
 #include "pcg1d_exact.cuh"
 #include "pcg2d.cuh"
+#include "pcgamg2d.cuh"
 #include "pcgchol2d.cuh"
 #include "realise.cuh"
 #include "vqpc.h"
@@ -116,6 +121,14 @@ struct vqpc_ctx {
   int64_t ch_ldL = 0, ch_ldLi = 0, ch_nnz = 0;
   int ch_cap = 0;
   int ch_S = 8;
+  // 2-D SA-AMG kind (pcgamg2d.cuh): host hierarchies (kept for vqpc_amg_level) and their device copy
+  bool amg = false;
+  std::vector<amg::Hierarchy> amg_h;
+  DBuf<int> amg_i;
+  DBuf<double> amg_d, amg_work;
+  DBuf<AmgHierD> amg_hd;
+  int amg_cv = 0;           // doubles of coarse-level scratch per CTA (max over centroids)
+  int64_t amg_entries = 0;  // stored hierarchy entries per centroid (mean), roofline accounting
   cudaStream_t aux = nullptr;              // chunks beyond the solve subset (overlap with the PCG)
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   DBuf<int> aflag;     // assign_mma candidate-list overflow flag
@@ -453,12 +466,57 @@ void run_pcgchol2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_
   launch_check(c);
 }
 
+void run_pcgamg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d_kflag, const int32_t* d_perm,
+                  const int32_t* d_labels, int64_t B, int64_t out_base, double eps, int max_iter, const int32_t* d_mia,
+                  int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x, int64_t solve_limit) {
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcgamg2d_kernel, AMG_T, 0));
+  if (per_sm < 1) throw ApiError{VQPC_CUDA_ERROR, "pcgamg2d kernel does not fit on an SM"};
+  const int64_t blocks = cap_groups(std::min<int64_t>(B, static_cast<int64_t>(per_sm) * c->sm_count));
+  const int64_t stride = static_cast<int64_t>(AMG_WORK) * c->n + c->amg_cv + 2;
+  c->amg_work.ensure(static_cast<size_t>(blocks) * stride);
+  c->counter.ensure(1);
+  CK(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->stream));
+  PcgAmgParams prm{};
+  prm.g = c->g2;
+  prm.kappa = d_kappa;
+  prm.ldk = ldk;
+  prm.kflag = d_kflag;
+  prm.perm = d_perm;
+  prm.labels = d_labels;
+  prm.hier = c->amg_hd.p;
+  prm.omega = 2.0 / 3.0;  // AmgOptions::jacobi_weight (solver.hpp:37)
+  prm.work = c->amg_work.p;
+  prm.cta_stride = stride;
+  prm.cv_off = AMG_WORK * c->n;
+  prm.B = B;
+  prm.out_base = out_base;
+  prm.solve_limit = solve_limit;
+  prm.eps = eps;
+  prm.max_iter = max_iter;
+  prm.max_iter_arr = d_mia;
+  prm.counter = c->counter.p;
+  prm.iters = d_iters;
+  prm.rel = d_rel;
+  prm.status = d_status;
+  prm.x_out = d_x;
+  prm.exact = c->exact;
+  Timed tm(c, VQPC_K_PCG);
+  pcgamg2d_kernel<<<static_cast<unsigned>(blocks), AMG_T, 0, c->stream>>>(prm);
+  launch_check(c);
+}
+
 void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d_kflag, const int32_t* d_perm,
                const int32_t* d_labels, int64_t B, int64_t out_base, double eps, int max_iter, const int32_t* d_mia,
                int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x, int64_t solve_limit) {
   if (c->chol2d) {
     run_pcgchol2d(c, d_kappa, ldk, d_kflag, d_perm, d_labels, B, out_base, eps, max_iter, d_mia, d_iters, d_rel,
                   d_status, d_x, solve_limit);
+    return;
+  }
+  if (c->amg) {
+    run_pcgamg2d(c, d_kappa, ldk, d_kflag, d_perm, d_labels, B, out_base, eps, max_iter, d_mia, d_iters, d_rel,
+                 d_status, d_x, solve_limit);
     return;
   }
   int per_sm = 0;
@@ -840,6 +898,145 @@ void setup_chol2d(vqpc_ctx* c) {
   CK(cudaStreamSynchronize(c->stream));
 }
 
+// 2-D SA-AMG kind: the centroid matrices' CSR rows are assembled on the device with
+// the oracle's operations (amg_centroid_rows_kernel), the P hierarchies are built on
+// host threads (amg_setup.cuh; independent per centroid, as the reference builds
+// each AmgPreconditioner, driver.cpp:212-219) and packed as sliced ELL.
+void setup_amg(vqpc_ctx* c, int64_t ldk) {
+  const int P = c->pb.P, n = c->n;
+  DBuf<double> rows;
+  rows.ensure(static_cast<size_t>(P) * n * 7);
+  amg_centroid_rows_kernel<<<4 * c->sm_count, 256, 0, c->stream>>>(c->kappa_c.p, ldk, P, c->g2, rows.p);
+  launch_check(c);
+  std::vector<double> hv(static_cast<size_t>(P) * n * 7);
+  d2h(c, hv.data(), rows.p, hv.size());
+  CK(cudaStreamSynchronize(c->stream));
+  rows.release();
+  c->amg_h.assign(P, {});
+  std::vector<int> failed(P, 0);
+  const int m = c->g2.m;
+  const int offs[7] = {-m - 1, -m, -1, 0, 1, m, m + 1};
+  auto work = [&](int p) {
+    amg::Csr A;
+    A.rows = A.cols = n;
+    A.ptr.assign(n + 1, 0);
+    A.idx.reserve(static_cast<size_t>(n) * 7);
+    A.val.reserve(static_cast<size_t>(n) * 7);
+    for (int i = 0; i < n; ++i) {
+      const double* v = hv.data() + (static_cast<size_t>(p) * n + i) * 7;
+      for (int k = 0; k < 7; ++k)
+        if (!std::isnan(v[k])) {
+          A.idx.push_back(i + offs[k]);
+          A.val.push_back(v[k]);
+        }
+      A.ptr[i + 1] = static_cast<int>(A.idx.size());
+    }
+    try {
+      c->amg_h[p] = amg::build(A);
+    } catch (const amg::NotSpd&) {
+      failed[p] = 1;
+    }
+  };
+  {
+    const int nt = std::max(1, std::min<int>(P, static_cast<int>(std::thread::hardware_concurrency())));
+    std::vector<std::thread> pool;
+    std::atomic<int> next{0};
+    for (int w = 0; w < nt; ++w)
+      pool.emplace_back([&] {
+        for (int p = next++; p < P; p = next++) work(p);
+      });
+    for (auto& th : pool) th.join();
+  }
+  for (int p = 0; p < P; ++p)
+    if (failed[p]) throw ApiError{VQPC_NOT_SPD, "not-spd (AMG hierarchy of centroid " + std::to_string(p) + ")"};
+  // pack: ints (slice offsets + columns) and doubles (values, inverse diagonals, dense L)
+  std::vector<int> hi;
+  std::vector<double> hd;
+  struct EllOff { size_t soff, col, val; };
+  auto pack_ell = [&](const amg::Csr& M) {
+    EllOff o{hi.size(), 0, 0};
+    const int ns = (M.rows + 31) / 32;
+    std::vector<int> soff(ns + 1, 0);
+    for (int s = 0; s < ns; ++s) {
+      int w = 0;
+      for (int i = 32 * s; i < std::min(M.rows, 32 * s + 32); ++i) w = std::max(w, M.ptr[i + 1] - M.ptr[i]);
+      soff[s + 1] = soff[s] + 32 * w;
+    }
+    hi.insert(hi.end(), soff.begin(), soff.end());
+    o.col = hi.size();
+    o.val = hd.size();
+    hi.resize(hi.size() + soff[ns], -1);
+    hd.resize(hd.size() + soff[ns], 0.0);
+    for (int i = 0; i < M.rows; ++i)
+      for (int k = 0; k < M.ptr[i + 1] - M.ptr[i]; ++k) {
+        const size_t e = soff[i >> 5] + 32 * static_cast<size_t>(k) + (i & 31);
+        hi[o.col + e] = M.idx[M.ptr[i] + k];
+        hd[o.val + e] = M.val[M.ptr[i] + k];
+      }
+    return o;
+  };
+  struct LevOff { EllOff A, P, Pt; size_t inv; };
+  std::vector<std::vector<LevOff>> lo(P);
+  std::vector<size_t> loff(P);
+  std::vector<AmgHierD> hh(P);
+  int cv_max = 0;
+  int64_t entries = 0;
+  for (int p = 0; p < P; ++p) {
+    const amg::Hierarchy& H = c->amg_h[p];
+    if (H.lv.size() > static_cast<size_t>(AMG_MAXLEV))
+      throw ApiError{VQPC_INVALID_CONFIG, "AMG hierarchy deeper than the device limit"};
+    if (H.dense_n > AMG_MAXDENSE) throw ApiError{VQPC_INVALID_CONFIG, "AMG coarsest level too large for the dense solve"};
+    int cv = 0;
+    for (size_t l = 0; l < H.lv.size(); ++l) {
+      const amg::Level& L = H.lv[l];
+      LevOff o{};
+      o.A = pack_ell(L.A);
+      if (L.P.rows) {
+        o.P = pack_ell(L.P);
+        o.Pt = pack_ell(L.Pt);
+      }
+      o.inv = hd.size();
+      hd.insert(hd.end(), L.inv_diag.begin(), L.inv_diag.end());
+      lo[p].push_back(o);
+      AmgLevelD& d = hh[p].lv[l];
+      d.n = L.A.rows;
+      d.nc = L.P.rows ? L.P.cols : 0;
+      d.voff = l == 0 ? 0 : cv;
+      if (l > 0) cv += 3 * d.n;
+      entries += L.A.nnz() + L.P.nnz() + L.Pt.nnz();
+    }
+    cv_max = std::max(cv_max, cv);
+    loff[p] = hd.size();
+    hd.insert(hd.end(), H.L.begin(), H.L.end());
+    hh[p].nlev = static_cast<int>(H.lv.size());
+    hh[p].dense_n = H.dense_n;
+  }
+  c->amg_i.ensure(hi.size());
+  c->amg_d.ensure(hd.size());
+  h2d(c, c->amg_i.p, hi.data(), hi.size());
+  h2d(c, c->amg_d.p, hd.data(), hd.size());
+  auto ell_ptr = [&](const EllOff& o) {
+    return AmgEll{c->amg_i.p + o.soff, c->amg_i.p + o.col, c->amg_d.p + o.val};
+  };
+  for (int p = 0; p < P; ++p) {
+    for (int l = 0; l < hh[p].nlev; ++l) {
+      AmgLevelD& d = hh[p].lv[l];
+      d.A = ell_ptr(lo[p][l].A);
+      if (d.nc) {
+        d.P = ell_ptr(lo[p][l].P);
+        d.Pt = ell_ptr(lo[p][l].Pt);
+      }
+      d.inv_diag = c->amg_d.p + lo[p][l].inv;
+    }
+    hh[p].L = c->amg_d.p + loff[p];
+  }
+  c->amg_hd.ensure(P);
+  h2d(c, c->amg_hd.p, hh.data(), P);
+  CK(cudaStreamSynchronize(c->stream));
+  c->amg_cv = (cv_max + 1) & ~1;
+  c->amg_entries = entries / P;
+}
+
 // The full campaign on device-resident arrays (run_campaign_with semantics).
 void campaign_device(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, double eps, int max_iter, int64_t chunk,
                      int32_t* d_labels, int32_t* d_iters, double* d_rel, uint8_t* d_status, int64_t* d_stats,
@@ -980,6 +1177,7 @@ int vqpc_unknowns(const vqpc_ctx* c) { return c ? c->n : 0; }
 int64_t vqpc_factor_entries(const vqpc_ctx* c) {
   if (!c) return 0;
   if (c->chol2d) return c->ch_nnz;
+  if (c->amg) return c->amg_entries;
   return c->pb.dim == 2 ? 3 * static_cast<int64_t>(c->n) : 2 * static_cast<int64_t>(c->n) - 1;
 }
 int64_t vqpc_launch_count(const vqpc_ctx* c) { return c ? c->launches : 0; }
@@ -997,7 +1195,8 @@ int vqpc_ctx_create(const vqpc_problem* pb, vqpc_ctx** out) {
   const bool grid = pb->method == VQPC_GRID || pb->method == VQPC_SIGN_GRID;
   if (grid && !pb->latent) return VQPC_INVALID_CODEBOOK;
   if (pb->dim == 1 && pb->precond != VQPC_PC_CHOLESKY) return VQPC_INVALID_CONFIG;
-  if (pb->dim == 2 && ((pb->precond != VQPC_PC_IC0 && pb->precond != VQPC_PC_CHOLESKY) || pb->size - 1 > P2_T))
+  if (pb->dim == 2 && ((pb->precond != VQPC_PC_IC0 && pb->precond != VQPC_PC_CHOLESKY && pb->precond != VQPC_PC_AMG) ||
+                       pb->size - 1 > P2_T))
     return VQPC_INVALID_CONFIG;
   auto* c = new vqpc_ctx();
   c->pb = *pb;
@@ -1018,6 +1217,7 @@ int vqpc_ctx_create(const vqpc_problem* pb, vqpc_ctx** out) {
       diag_orders(dp);
       CK(cudaMemcpyToSymbol(vqpc_dperm, dp, sizeof(dp)));
       if (pb->precond == VQPC_PC_CHOLESKY) setup_chol2d(c);
+      c->amg = pb->precond == VQPC_PC_AMG;
     }
     if (pb->dim == 1) {
       const PcgVariant* v = pick_pcg(c->n);
@@ -1085,6 +1285,10 @@ void vqpc_ctx_destroy(vqpc_ctx* c) {
   c->ch_groups.release();
   c->ch_perm.release();
   for (auto* b : {&c->ch_L, &c->ch_Linv, &c->ch_work}) b->release();
+  c->amg_i.release();
+  c->amg_d.release();
+  c->amg_work.release();
+  c->amg_hd.release();
   if (c->aux) cudaStreamDestroy(c->aux);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
@@ -1163,6 +1367,8 @@ int vqpc_factor_centroids(vqpc_ctx* c) {
         CK(cudaMemcpy2DAsync(c->ch_Linv.p + static_cast<size_t>(p) * c->ch_ldLi + PC_STG_META, PC_LIB * sizeof(double),
                              c->ch_bmeta.p, 2 * PC_BS * sizeof(int), 2 * PC_BS * sizeof(int), c->clay.nblk,
                              cudaMemcpyDeviceToDevice, c->stream));
+    } else if (pb.dim == 2 && c->amg) {
+      setup_amg(c, ldk);
     } else if (pb.dim == 2) {
       c->fac2.ensure(static_cast<size_t>(P) * P2_FAC * c->n);
       Timed tm(c, VQPC_K_OTHER);
@@ -1209,7 +1415,12 @@ int vqpc_precond_apply(vqpc_ctx* c, int p, const double* r, double* z) {
     if (p < 0 || p >= c->pb.P) throw ApiError{VQPC_INVALID_ARGUMENT, "p out of range"};
     c->dvec.ensure(3 * static_cast<size_t>(c->n));
     h2d(c, c->dvec.p, r, c->n);
-    if (c->chol2d)
+    if (c->amg) {
+      c->dvec.ensure(5 * static_cast<size_t>(c->n) + c->amg_cv);
+      h2d(c, c->dvec.p, r, c->n);
+      amg_apply_kernel<<<1, AMG_T, 0, c->stream>>>(c->amg_hd.p, p, 2.0 / 3.0, c->dvec.p, c->dvec.p + c->n,
+                                                   c->dvec.p + 2 * c->n, c->dvec.p + 3 * c->n, c->dvec.p + 5 * c->n);
+    } else if (c->chol2d)
       cholapply_serial_kernel<<<1, 1, 0, c->stream>>>(c->ch_L.p, c->ch_ldL, c->clay, p, c->dvec.p,
                                                       c->dvec.p + 2 * c->n, c->dvec.p + c->n);
     else if (c->pb.dim == 2)
@@ -1221,6 +1432,43 @@ int vqpc_precond_apply(vqpc_ctx* c, int p, const double* r, double* z) {
     d2h(c, z, c->dvec.p + c->n, c->n);
     CK(cudaStreamSynchronize(c->stream));
   });
+}
+
+// SA-AMG hierarchy of centroid p (AmgOptions::level_sizes_out, solver.hpp:42, and
+// the operators, for bit-level checks against the oracle's setup)
+int vqpc_amg_info(const vqpc_ctx* c, int p, int max_levels, int64_t* info, int* nlev, int* dense_n) {
+  if (!c || !info || !nlev || !dense_n) return VQPC_INVALID_ARGUMENT;
+  if (!c->amg || c->amg_h.empty()) return VQPC_INVALID_CONFIG;
+  if (p < 0 || p >= c->pb.P) return VQPC_INVALID_ARGUMENT;
+  const amg::Hierarchy& H = c->amg_h[p];
+  *nlev = static_cast<int>(H.lv.size());
+  *dense_n = H.dense_n;
+  for (int l = 0; l < *nlev && l < max_levels; ++l) {
+    info[4 * l] = H.lv[l].A.rows;
+    info[4 * l + 1] = H.lv[l].A.nnz();
+    info[4 * l + 2] = H.lv[l].P.nnz();
+    info[4 * l + 3] = H.lv[l].P.rows ? H.lv[l].P.cols : 0;
+  }
+  return VQPC_OK;
+}
+
+int vqpc_amg_level(const vqpc_ctx* c, int p, int l, int* a_rp, int* a_col, double* a_val, double* inv_diag,
+                   int* p_rp, int* p_col, double* p_val, double* L) {
+  if (!c || !c->amg || c->amg_h.empty()) return VQPC_INVALID_CONFIG;
+  if (p < 0 || p >= c->pb.P || l < 0 || l >= static_cast<int>(c->amg_h[p].lv.size())) return VQPC_INVALID_ARGUMENT;
+  const amg::Hierarchy& H = c->amg_h[p];
+  const amg::Level& lv = H.lv[l];
+  std::copy(lv.A.ptr.begin(), lv.A.ptr.end(), a_rp);
+  std::copy(lv.A.idx.begin(), lv.A.idx.end(), a_col);
+  std::copy(lv.A.val.begin(), lv.A.val.end(), a_val);
+  std::copy(lv.inv_diag.begin(), lv.inv_diag.end(), inv_diag);
+  if (lv.P.rows) {
+    std::copy(lv.P.ptr.begin(), lv.P.ptr.end(), p_rp);
+    std::copy(lv.P.idx.begin(), lv.P.idx.end(), p_col);
+    std::copy(lv.P.val.begin(), lv.P.val.end(), p_val);
+  }
+  if (L && l + 1 == static_cast<int>(H.lv.size())) std::copy(H.L.begin(), H.L.end(), L);
+  return VQPC_OK;
 }
 
 int vqpc_assign_d(vqpc_ctx* c, const double* d_xi, int64_t B, int ld, int32_t* d_labels) {

@@ -78,6 +78,8 @@ def load():
             "vqpc_debug_pcg2d_phase_cycles": (I, [C.POINTER(C.c_ulonglong), I]),
             "vqpc_debug_pcg1d_phase_cycles": (I, [C.POINTER(C.c_ulonglong), I]),
             "vqpc_counter_hash": (U64, [U64, U64, U64]),
+            "vqpc_amg_info": (I, [VP, I, I, VP, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+            "vqpc_amg_level": (I, [VP, I, I, VP, VP, VP, VP, VP, VP, VP, VP]),
             "vqpc_normal_quantile": (D, [D]),
         }
         for name, (res, args) in sig.items():
@@ -231,6 +233,32 @@ class Context:
     def factor_centroids(self):
         self._c(load().vqpc_factor_centroids(self.h))
         self.factored = True
+        self.factor_entries = int(load().vqpc_factor_entries(self.h))
+
+    def amg_levels(self, p):
+        """SA-AMG hierarchy of centroid p as built by the library (same layout as
+        oracle.PreconditionerSet.amg_levels)."""
+        info = np.zeros(4 * 64, np.int64)
+        nlev, dn = C.c_int(), C.c_int()
+        self._c(load().vqpc_amg_info(self.h, p, 64, _p(info), C.byref(nlev), C.byref(dn)))
+        out = []
+        for l in range(nlev.value):
+            n, nnz, pnnz, nc = (int(v) for v in info[4 * l:4 * l + 4])
+            a_rp, a_col, a_val = np.empty(n + 1, np.int32), np.empty(nnz, np.int32), np.empty(nnz)
+            inv = np.empty(n)
+            p_rp = np.empty(n + 1, np.int32) if pnnz else np.empty(1, np.int32)
+            p_col, p_val = np.empty(max(pnnz, 1), np.int32), np.empty(max(pnnz, 1))
+            last = l + 1 == nlev.value
+            L = np.empty(dn.value * dn.value) if last and dn.value else None
+            self._c(load().vqpc_amg_level(self.h, p, l, _p(a_rp), _p(a_col), _p(a_val), _p(inv), _p(p_rp),
+                                          _p(p_col), _p(p_val), _p(L) if L is not None else None))
+            lv = dict(n=n, A=(a_rp, a_col, a_val), inv_diag=inv, nc=nc)
+            if pnnz:
+                lv["P"] = (p_rp, p_col[:pnnz], p_val[:pnnz])
+            if L is not None:
+                lv["L"] = L.reshape(dn.value, dn.value)
+            out.append(lv)
+        return out
 
     def centroid_coefficients(self):
         out = np.empty((self.P, self.n_nodes))

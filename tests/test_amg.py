@@ -1,0 +1,170 @@
+"""SA-AMG, the reference's default preconditioner kind (PrecondKind::Amg,
+driver.hpp:36; amg.cpp:40-230): the oracle's restatement (CPU) and the GPU
+library's own hierarchy + V-cycle kernel against it.
+
+CPU: hierarchy properties of the oracle (coarsening until <= coarse_size rows,
+Galerkin operators symmetric to rounding and positive definite, prolongator
+damping, V-cycle SPD as an operator), and that AMG-preconditioned PCG converges
+in far fewer iterations than IC(0) on the same mesh (the paper's premise).
+GPU: the library's setup (host threads, amg_setup.cuh) builds the SAME
+hierarchy bit for bit; the device V-cycle equals the oracle's apply bit for
+bit; reference-order PCG is bit-identical; the fast mode's J statistics sit
+within the oracle's own FMA spread.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2403_07824_b200 import campaign
+from tests.conftest import HAS_GPU
+from tests.helpers import CONFIGS, compare_runs, oracle_codebook, setup_case
+
+CONFIGS.setdefault("C4amgs", campaign.scaled(campaign.CONFIGS["C4amg"], mesh_resolution=32, name="C4amgs"))
+
+
+def _csr(lv, key="A"):
+    rp, col, val = lv[key]
+    n = len(rp) - 1
+    return rp, col, val, n
+
+
+def _dense(lv, key="A", ncols=None):
+    rp, col, val, n = _csr(lv, key)
+    M = np.zeros((n, ncols or n))
+    for i in range(n):
+        M[i, col[rp[i]:rp[i + 1]]] += val[rp[i]:rp[i + 1]]
+    return M
+
+
+def test_oracle_amg_hierarchy_properties():
+    cfg, basis, cb, xi = setup_case("C4amgs", 8)
+    ps = oracle.PreconditionerSet.build(2, cfg["mesh_resolution"], "amg", oracle_codebook(cb), basis["eigenvalues"],
+                                        basis["eigenvectors"])
+    lv = ps.amg_levels(0)
+    sizes = [l["n"] for l in lv]
+    assert sizes[0] == 31 * 31 and all(a > b for a, b in zip(sizes, sizes[1:]))
+    assert sizes[-1] <= 64 and len(sizes) >= 2  # coarsened to a dense coarsest level (amg.cpp:146, 186)
+    for l, nxt in zip(lv[:-1], lv[1:]):
+        A = _dense(l)
+        P = _dense(l, "P", l["nc"])
+        Ac = P.T @ A @ P
+        assert np.allclose(Ac, _dense(nxt), rtol=1e-12, atol=1e-12 * np.abs(Ac).max())  # Galerkin
+        assert np.array_equal(1.0 / np.diag(A), l["inv_diag"])
+    Lc = lv[-1]["L"]
+    Acoarse = _dense(lv[-1])
+    assert np.allclose(Lc @ Lc.T, np.tril(Acoarse) + np.tril(Acoarse, -1).T, rtol=1e-12)
+    # the V-cycle is a symmetric positive definite operator
+    n = sizes[0]
+    rng = np.random.default_rng(0)
+    M = np.stack([ps.apply(0, e) for e in np.eye(n)[:: max(1, n // 64)]])
+    idx = np.arange(0, n, max(1, n // 64))
+    Ms = M[:, idx]
+    assert np.allclose(Ms, Ms.T, rtol=1e-9, atol=1e-12 * np.abs(Ms).max())
+    for _ in range(4):
+        r = rng.standard_normal(n)
+        assert r @ ps.apply(0, r) > 0
+
+
+def test_oracle_amg_converges_faster_than_ic0():
+    cfg, basis, cb, xi = setup_case("C4amgs", 32)
+    args = (2, cfg["mesh_resolution"])
+    ocb = oracle_codebook(cb)
+    amg = oracle.run_campaign(*args, "amg", ocb, basis["eigenvalues"], basis["eigenvectors"], xi, cfg["eps"])
+    ic0 = oracle.run_campaign(*args, "ic0", ocb, basis["eigenvalues"], basis["eigenvectors"], xi, cfg["eps"])
+    assert (amg["status"] == 0).all() and (ic0["status"] == 0).all()
+    assert amg["iterations"].mean() < ic0["iterations"].mean()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,ps", [("C4amgs", None), ("C4amg", [0, 7, 31])])
+def test_gpu_amg_hierarchy_bit_identical(name, ps):
+    """The library's own setup (amg_setup.cuh, host threads, centroid rows assembled on
+    the device) builds exactly the oracle's hierarchy: every level's operator,
+    inverse diagonal, prolongator and the coarsest dense factor, bit for bit."""
+    cfg, basis, cb, xi = setup_case(name, 4)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    kc = ctx.centroid_coefficients()
+    ops = oracle.PreconditionerSet.from_coefficients(2, cfg["mesh_resolution"], "amg", kc)
+    for p in (ps or range(cb["P"])):
+        g, o = ctx.amg_levels(p), ops.amg_levels(p)
+        assert [l["n"] for l in g] == [l["n"] for l in o], p
+        for lg, lo in zip(g, o):
+            for k in ("A", "P"):
+                if k in lo:
+                    for a, b in zip(lg[k], lo[k]):
+                        assert np.array_equal(a, b), (p, k)
+            assert np.array_equal(lg["inv_diag"], lo["inv_diag"])
+        assert np.array_equal(g[-1]["L"], o[-1]["L"])
+    print(name, "hierarchy:", [l["n"] for l in ctx.amg_levels(0)])
+    ctx.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["C4amgs", "C4amg"])
+def test_gpu_amg_apply_bit_identical(name):
+    """One V-cycle on the device (amg_vcycle) equals the oracle's apply bit for bit."""
+    cfg, basis, cb, xi = setup_case(name, 4)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    kc = ctx.centroid_coefficients()
+    ops = oracle.PreconditionerSet.from_coefficients(2, cfg["mesh_resolution"], "amg", kc)
+    rng = np.random.default_rng(5)
+    for p in (0, cb["P"] - 1):
+        r = rng.standard_normal(ctx.n)
+        assert np.array_equal(ctx.precond_apply(p, r), ops.apply(p, r)), p
+    ctx.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,n", [("C4amgs", 48), ("C4amg", 16)])
+def test_gpu_amg_exact_mode_bit_identical(name, n):
+    """Reference-order mode: J, status, final residual and x bit-identical to the
+    oracle's pcg with its AMG preconditioner (same coefficient bits)."""
+    cfg, basis, cb, xi = setup_case(name, n)
+    ocb = oracle_codebook(cb)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    ctx.set_exact_reductions(True)
+    kc = ctx.centroid_coefficients()
+    labels = oracle.assign(ocb, xi)
+    kap, _ = ctx.realise(xi)
+    it, rel, st, x = ctx.solve_batch(xi, labels, cfg["eps"], want_x=True)
+    ctx.close()
+    ops = oracle.PreconditionerSet.from_coefficients(2, cfg["mesh_resolution"], "amg", kc)
+    for i in range(n):
+        out = ops.pcg(int(labels[i]), kap[i], cfg["eps"])
+        assert out["iterations"] == it[i] and out["status"] == st[i], (i, out["iterations"], it[i])
+        assert out["rel"] == rel[i], i
+        assert np.array_equal(out["x"], x[i]), i
+    print(name, "AMG exact mode: %d samples bit-identical, mean J %.2f" % (n, it.mean()))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,n", [("C4amgs", 256), ("C4amg", 128)])
+def test_gpu_amg_campaign_parity(name, n):
+    """Fast mode (block-tree dots) vs the oracle's run_campaign_with, beside the
+    oracle's own FMA build: bit-exact labels, identical statuses, J spread within
+    the yardstick's."""
+    import os
+    cfg, basis, cb, xi = setup_case(name, n)
+    ocb = oracle_codebook(cb)
+    res = campaign.run_campaign_with(cfg, dict(basis=basis, codebook=cb), xi)
+    args = (2, cfg["mesh_resolution"], "amg", ocb, basis["eigenvalues"], basis["eigenvectors"], xi, cfg["eps"])
+    ref = oracle.run_campaign(*args, threads=os.cpu_count())
+    with oracle.fma_variant():
+        fma = oracle.run_campaign(*args, threads=os.cpu_count())
+    assert np.array_equal(res["labels"], ref["labels"])
+    cmp = compare_runs(ref["iterations"], ref["status"], res["iterations"], res["status"])
+    yard = compare_runs(ref["iterations"], ref["status"], fma["iterations"], fma["status"])
+    print(name, "AMG gpu:", {k: v for k, v in cmp.items() if k != "disagree"}, "fma-yardstick:",
+          {k: v for k, v in yard.items() if k != "disagree"})
+    assert cmp["status_agree"] == 1.0
+    assert cmp["max_dj"] <= max(2, 2 * yard["max_dj"])
+    assert abs(cmp["mean_cpu"] - cmp["mean_gpu"]) <= max(3 * abs(yard["mean_cpu"] - yard["mean_gpu"]), 0.05)
+
+
+@pytest.mark.skipif(HAS_GPU, reason="CPU-only check")
+def test_amg_kind_without_device():
+    from paper_2403_07824_b200 import lib
+    cfg, basis, cb, xi = setup_case("C4amgs", 4)
+    with pytest.raises(lib.VqpcError) as e:
+        campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    assert "no-device" in str(e.value)
