@@ -389,10 +389,13 @@ static std::vector<int> rcm_permutation(const Csr& A) {
 // off-diagonal L_kl = (B_kl - sum_j L_kj L_lj) / L_ll and the pivot
 // L_kk = sqrt(B_kk - sum_j L_kj^2) (Eigen SimplicialLLT's up-looking rows; on
 // tridiagonal matrices the arithmetic is identical). Solves follow Eigen's
-// sparse triangular solves: forward subtracts column contributions in
-// increasing column order, then divides by the pivot; backward likewise.
+// sparse triangular solves (SimplicialCholeskyBase::_solve_impl): forward with
+// the column-major lower factor (each y_k receives its column contributions in
+// increasing column order, then the division by the pivot), backward with the
+// row-major upper view L^T (row by row from the bottom, each row's stored
+// entries in increasing column order).
 struct CholeskyPreconditioner final : Preconditioner {
-  int n = 0;
+  int n = 0, W = 0;
   std::vector<int> perm, first;    // envelope start per permuted row
   std::vector<size_t> start;       // offset of row k in L (entries first[k]..k)
   std::vector<double> L;
@@ -409,6 +412,7 @@ struct CholeskyPreconditioner final : Preconditioner {
     }
     start.assign(n + 1, 0);
     for (int k = 0; k < n; ++k) start[k + 1] = start[k] + static_cast<size_t>(k - first[k] + 1);
+    for (int k = 0; k < n; ++k) W = std::max(W, k - first[k]);
     L.assign(start[n], 0.0);
     for (int k = 0; k < n; ++k) {
       double* Lk = L.data() + start[k] - first[k];  // Lk[l] = L(k, l)
@@ -439,11 +443,20 @@ struct CholeskyPreconditioner final : Preconditioner {
       for (int j = first[k]; j < k; ++j) t -= y[j] * Lk[j];
       y[k] = t / Lk[k];
     }
-    for (int k = n - 1; k >= 0; --k) {  // L^T z = y (column-oriented)
-      const double* Lk = L.data() + start[k] - first[k];
-      const double zk = y[k] / Lk[k];
-      y[k] = zk;
-      for (int j = first[k]; j < k; ++j) y[j] -= Lk[j] * zk;
+    // L^T z = y as Eigen evaluates it: SimplicialLLT::solve applies matrixU() =
+    // L.adjoint(), an upper-triangular ROW-major view of the column-major factor, so
+    // the sparse triangular solve goes row by row from the bottom: z_i = (y_i -
+    // L(j1,i) z_j1 - L(j2,i) z_j2 - ...) / L(i,i) over the stored column i of L in
+    // ascending j (sequential subtraction). Row j holds column i iff first[j] <= i,
+    // and j - first[j] <= W bounds the scan.
+    for (int i = n - 1; i >= 0; --i) {
+      double t = y[i];
+      const int jmax = std::min(n - 1, i + W);
+      for (int j = i + 1; j <= jmax; ++j) {
+        if (first[j] > i) continue;
+        t -= L[start[j] - first[j] + i] * y[j];
+      }
+      y[i] = t / L[start[i] - first[i] + i];
     }
     for (int k = 0; k < n; ++k) z[perm[k]] = y[k];
   }

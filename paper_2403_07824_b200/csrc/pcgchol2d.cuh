@@ -144,21 +144,68 @@ __global__ void cholinv_kernel(const double* L, int64_t ldL, const CholLayout la
 // Work groups: up to S consecutive entries of a label bucket (perm is label-major,
 // predicted-cost-descending inside a bucket). Emitted q-major — the q-th group of
 // every label before any (q+1)-th — so every factor's heaviest samples go first.
-__global__ void chol_groups_kernel(const int64_t* offsets, int P, int S, int2* groups, int* ngroups) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int ng = 0;
+// One CTA: per round q, the labels whose bucket still has a q-th group are
+// compacted by a block-wide exclusive scan over the P + 1 buckets (O(P / CG_T)
+// per round instead of a serial O(P) loop).
+constexpr int CG_T = 1024;
+constexpr int CG_PER = 8;  // buckets per thread per scan (P + 1 <= CG_T * CG_PER handled per chunk)
+__global__ void __launch_bounds__(CG_T) chol_groups_kernel(const int64_t* offsets, int P, int S, int2* groups,
+                                                           int* ngroups) {
+  __shared__ int wsum[CG_T / 32];
+  __shared__ int s_base, s_any;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (t == 0) s_base = 0;
+  __syncthreads();
   for (int64_t q = 0;; ++q) {
-    bool any = false;
-    for (int p = 0; p <= P; ++p) {
-      const int64_t lo = offsets[p] + q * S, hi = offsets[p + 1];
-      if (lo < hi) {
-        groups[ng++] = make_int2(static_cast<int>(lo), static_cast<int>(hi - lo < S ? hi - lo : S));
-        any = true;
+    if (t == 0) s_any = 0;
+    __syncthreads();
+    for (int c0 = 0; c0 <= P; c0 += CG_T * CG_PER) {
+      int cnt = 0;
+      bool has[CG_PER];
+#pragma unroll
+      for (int u = 0; u < CG_PER; ++u) {
+        const int p = c0 + t * CG_PER + u;
+        has[u] = p <= P && offsets[p] + q * S < offsets[p + 1];
+        cnt += has[u];
       }
+      int incl = cnt;  // inclusive scan of cnt over the block
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += v;
+      }
+      if (lane == 31) wsum[warp] = incl;
+      __syncthreads();
+      if (warp == 0) {
+        int w = lane < CG_T / 32 ? wsum[lane] : 0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, w, off);
+          if (lane >= off) w += v;
+        }
+        if (lane < CG_T / 32) wsum[lane] = w;  // inclusive over warps
+      }
+      __syncthreads();
+      int pos = s_base + (warp > 0 ? wsum[warp - 1] : 0) + incl - cnt;
+#pragma unroll
+      for (int u = 0; u < CG_PER; ++u) {
+        const int p = c0 + t * CG_PER + u;
+        if (has[u]) {
+          const int64_t lo = offsets[p] + q * S, hi = offsets[p + 1];
+          groups[pos++] = make_int2(static_cast<int>(lo), static_cast<int>(hi - lo < S ? hi - lo : S));
+        }
+      }
+      const int total = wsum[CG_T / 32 - 1];
+      __syncthreads();
+      if (t == 0) {
+        s_base += total;
+        if (total) s_any = 1;
+      }
+      __syncthreads();
     }
-    if (!any) break;
+    if (!s_any) break;
   }
-  *ngroups = ng;
+  if (t == 0) *ngroups = s_base;
 }
 
 struct PcholParams {
@@ -527,6 +574,10 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
               }
             }
           }
+          // these generic-proxy writes to the ring precede later cp.async.bulk writes of
+          // the same rows (the zin reloads): order them for the async proxy before the
+          // barrier that releases the next issue
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncthreads();
         }
         P2_TIC(t_iss);
@@ -716,14 +767,16 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
   }
 }
 
-// Preconditioner::apply for one centroid in the oracle's serial order (tests):
-// y = L^-1 P r row by row, then L^T z = y column by column (one thread).
-__global__ void cholapply_serial_kernel(const double* L, int64_t ldL, const CholLayout lay, int p,
-                                        const double* r, double* y, double* z) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const double* Lp = L + static_cast<size_t>(p) * ldL;
+// Preconditioner::apply for one centroid in the reference's serial order:
+// Eigen's SimplicialLLT solve (solver.cpp:99-105; SimplicialCholeskyBase::_solve_impl)
+// on the RCM-permuted vector. Forward: the column-major lower factor, every y_k
+// receiving its column contributions in increasing column order. Backward:
+// matrixU() = L.adjoint(), a row-major upper view, solved row by row from the
+// bottom, z_i = (y_i - L(j1,i) z_j1 - L(j2,i) z_j2 - ...) / L(i,i) with j
+// ascending over column i's stored rows (first[j] <= i, j - first[j] <= W).
+// y is overwritten by z; one thread (the instrument, not the throughput path).
+__device__ void chol_serial_solve(const double* Lp, const CholLayout& lay, double* y) {
   const int n = lay.n;
-  for (int k = 0; k < n; ++k) y[k] = r[lay.cperm[k]];
   for (int k = 0; k < n; ++k) {
     const int f = lay.first[k];
     const double* Lk = Lp + lay.start[k] - f;
@@ -731,14 +784,169 @@ __global__ void cholapply_serial_kernel(const double* L, int64_t ldL, const Chol
     for (int j = f; j < k; ++j) s = __dsub_rn(s, __dmul_rn(y[j], Lk[j]));
     y[k] = __ddiv_rn(s, Lk[k]);
   }
-  for (int k = n - 1; k >= 0; --k) {
-    const int f = lay.first[k];
-    const double* Lk = Lp + lay.start[k] - f;
-    const double zk = __ddiv_rn(y[k], Lk[k]);
-    y[k] = zk;
-    for (int j = f; j < k; ++j) y[j] = __dsub_rn(y[j], __dmul_rn(Lk[j], zk));
+  for (int i = n - 1; i >= 0; --i) {
+    double s = y[i];
+    const int jmax = min(n - 1, i + lay.W);
+    for (int j = i + 1; j <= jmax; ++j) {
+      const int fj = lay.first[j];
+      if (fj > i) continue;
+      s = __dsub_rn(s, __dmul_rn(Lp[lay.start[j] - fj + i], y[j]));
+    }
+    y[i] = __ddiv_rn(s, Lp[lay.start[i] - lay.first[i] + i]);
   }
+}
+
+__global__ void cholapply_serial_kernel(const double* L, int64_t ldL, const CholLayout lay, int p,
+                                        const double* r, double* y, double* z) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double* Lp = L + static_cast<size_t>(p) * ldL;
+  const int n = lay.n;
+  for (int k = 0; k < n; ++k) y[k] = r[lay.cperm[k]];
+  chol_serial_solve(Lp, lay, y);
   for (int k = 0; k < n; ++k) z[lay.cperm[k]] = y[k];
+}
+
+// Reference-order mode of the 2-D cholesky kind (vqpc_set_exact_reductions): one CTA
+// per sample; the vector passes are the throughput kernel's (same operations), the
+// dot products are summed serially in NATURAL order (solver.cpp:176-180) from
+// products stored at their natural index, and the preconditioner is
+// chol_serial_solve. Given the same coefficient bits the whole solve (J, status,
+// residual record, x) is bit-identical to the oracle. A parity instrument: the
+// serial triangular solves cost ~n W dependent operations per application.
+constexpr int PCX_NV = 13;  // D, cS, cW, cE, cN, b, x, r, p, Ap, z, prod, (spare)
+__global__ void __launch_bounds__(PC_T) pcgchol2d_exact_kernel(const PcholParams prm) {
+  __shared__ double s_val;
+  __shared__ int64_t s_item;
+  const Grid2D g = prm.g;
+  const CholLayout lay = prm.lay;
+  const int n = lay.n, t = threadIdx.x;
+  double* base = prm.work + static_cast<size_t>(blockIdx.x) * PCX_NV * prm.ldv;
+  auto vec = [&](int v) { return base + static_cast<size_t>(v) * prm.ldv; };
+  double *D = vec(0), *CS = vec(1), *CW = vec(2), *CE = vec(3), *CN = vec(4), *Bv = vec(5), *X = vec(6), *R = vec(7),
+         *Pv = vec(8), *AP = vec(9), *Z = vec(10), *Prod = vec(11);
+  auto serial = [&]() {  // s = 0; s += prod_i, natural order
+    __syncthreads();
+    if (t == 0) {
+      double acc = 0.0;
+      for (int i = 0; i < n; ++i) acc = __dadd_rn(acc, Prod[i]);
+      s_val = acc;
+    }
+    __syncthreads();
+    const double v = s_val;
+    __syncthreads();
+    return v;
+  };
+  for (;;) {
+    if (t == 0) s_item = atomicAdd(prm.counter, 1);
+    __syncthreads();
+    const int64_t item = s_item;
+    __syncthreads();
+    if (item >= prm.B) break;
+    const int sm = prm.perm[item];
+    const int64_t gs = prm.out_base + sm;
+    const int label = prm.labels[sm];
+    if (label < 0 || prm.kflag[sm] || gs >= prm.solve_limit) {
+      if (t == 0) {
+        prm.iters[gs] = 0;
+        prm.rel[gs] = 0.0;
+        prm.status[gs] = gs >= prm.solve_limit ? VQPC_S_NOT_SOLVED
+                         : label < 0           ? VQPC_S_INVALID_LATENT
+                                               : (prm.kflag[sm] & 1) ? VQPC_S_COEFF_OVERFLOW : VQPC_S_INVALID_COEFF;
+      }
+      continue;
+    }
+    const double* Lp = prm.L + static_cast<size_t>(label) * prm.ldL;
+    const double* kap = prm.kappa + static_cast<size_t>(sm) * prm.ldk;
+    const int max_iter = prm.max_iter_arr ? prm.max_iter_arr[gs] : (prm.max_iter < 0 ? 10 * n : prm.max_iter);
+    for (int k = t; k < n; k += PC_T) {
+      const int id = lay.cperm[k];
+      const RowCoef rc = assemble_row(kap, g, id % g.m, id / g.m);
+      D[k] = rc.d;
+      CS[k] = rc.s;
+      CW[k] = rc.w;
+      CE[k] = rc.e;
+      CN[k] = rc.nn;
+      Bv[k] = rc.b;
+      X[k] = 0.0;
+      R[k] = rc.b;
+      Z[k] = rc.b;
+      Prod[id] = __dmul_rn(rc.b, rc.b);
+    }
+    const double norm_b = sqrt(serial());
+    if (t == 0) chol_serial_solve(Lp, lay, Z);
+    __syncthreads();
+    for (int k = t; k < n; k += PC_T) {
+      Pv[k] = Z[k];
+      Prod[lay.cperm[k]] = __dmul_rn(R[k], Z[k]);
+    }
+    double rz = serial();
+    int J = 0;
+    double rel_rec = 0.0;
+    uint8_t st = VQPC_S_MAX_ITER;
+    if (norm_b == 0.0) st = VQPC_S_CONVERGED;
+    else if (!(rz > 0.0)) st = VQPC_S_BREAKDOWN;
+    else {
+      for (int j = 1; j <= max_iter; ++j) {
+        for (int k = t; k < n; k += PC_T) {
+          const int4 nb = lay.nbr[k];
+          const double ap = row_apply(CS[k], CW[k], D[k], CE[k], CN[k], nb.x >= 0 ? Pv[nb.x] : 0.0,
+                                      nb.y >= 0 ? Pv[nb.y] : 0.0, Pv[k], nb.z >= 0 ? Pv[nb.z] : 0.0,
+                                      nb.w >= 0 ? Pv[nb.w] : 0.0);
+          AP[k] = ap;
+          Prod[lay.cperm[k]] = __dmul_rn(Pv[k], ap);
+        }
+        const double pAp = serial();
+        if (!(pAp > 0.0)) {
+          st = VQPC_S_BREAKDOWN;
+          break;
+        }
+        const double alpha = rz / pAp;
+        for (int k = t; k < n; k += PC_T) {
+          X[k] = __dadd_rn(X[k], __dmul_rn(alpha, Pv[k]));
+          R[k] = __dsub_rn(R[k], __dmul_rn(alpha, AP[k]));
+        }
+        __syncthreads();
+        for (int k = t; k < n; k += PC_T) {
+          const int4 nb = lay.nbr[k];
+          const double ax = row_apply(CS[k], CW[k], D[k], CE[k], CN[k], nb.x >= 0 ? X[nb.x] : 0.0,
+                                      nb.y >= 0 ? X[nb.y] : 0.0, X[k], nb.z >= 0 ? X[nb.z] : 0.0,
+                                      nb.w >= 0 ? X[nb.w] : 0.0);
+          const double rt = __dsub_rn(Bv[k], ax);
+          Prod[lay.cperm[k]] = __dmul_rn(rt, rt);
+          Z[k] = R[k];
+        }
+        const double rel = sqrt(serial()) / norm_b;
+        J = j;
+        rel_rec = rel;
+        if (rel < prm.eps) {
+          st = VQPC_S_CONVERGED;
+          break;
+        }
+        if (t == 0) chol_serial_solve(Lp, lay, Z);
+        __syncthreads();
+        for (int k = t; k < n; k += PC_T) Prod[lay.cperm[k]] = __dmul_rn(R[k], Z[k]);
+        const double rz_next = serial();
+        if (!(rz_next > 0.0)) {
+          st = VQPC_S_BREAKDOWN;
+          break;
+        }
+        const double beta = rz_next / rz;
+        rz = rz_next;
+        for (int k = t; k < n; k += PC_T) Pv[k] = __dadd_rn(Z[k], __dmul_rn(beta, Pv[k]));
+        __syncthreads();
+      }
+    }
+    if (t == 0) {
+      prm.iters[gs] = J;
+      prm.rel[gs] = rel_rec;
+      prm.status[gs] = st;
+    }
+    if (prm.x_out) {
+      double* xo = prm.x_out + static_cast<size_t>(gs) * n;
+      for (int k = t; k < n; k += PC_T) xo[lay.cperm[k]] = X[k];
+    }
+    __syncthreads();
+  }
 }
 
 }  // namespace vqpc

@@ -405,8 +405,41 @@ void run_pcgchol2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_
                    const int32_t* d_labels, int64_t B, int64_t out_base, double eps, int max_iter,
                    const int32_t* d_mia, int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x,
                    int64_t solve_limit) {
-  if (c->exact) throw ApiError{VQPC_INVALID_CONFIG, "reference-order mode is not available for the 2-D cholesky kind"};
   const int P = c->pb.P, S = c->ch_S, n = c->n;
+  if (c->exact) {  // reference-order instrument: one CTA per sample, serial solves and dots
+    const int ldv = static_cast<int>(ceil_div(n, PC_BS) * PC_BS);
+    const int64_t blocks = cap_groups(std::min<int64_t>(B, 2LL * c->sm_count));
+    c->ch_work.ensure(static_cast<size_t>(blocks) * PCX_NV * ldv);
+    c->counter.ensure(1);
+    CK(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->stream));
+    PcholParams prm{};
+    prm.g = c->g2;
+    prm.lay = c->clay;
+    prm.kappa = d_kappa;
+    prm.ldk = ldk;
+    prm.kflag = d_kflag;
+    prm.perm = d_perm;
+    prm.labels = d_labels;
+    prm.L = c->ch_L.p;
+    prm.ldL = c->ch_ldL;
+    prm.ldv = ldv;
+    prm.work = c->ch_work.p;
+    prm.B = B;
+    prm.out_base = out_base;
+    prm.solve_limit = solve_limit;
+    prm.eps = eps;
+    prm.max_iter = max_iter;
+    prm.max_iter_arr = d_mia;
+    prm.counter = c->counter.p;
+    prm.iters = d_iters;
+    prm.rel = d_rel;
+    prm.status = d_status;
+    prm.x_out = d_x;
+    Timed tm(c, VQPC_K_PCG);
+    pcgchol2d_exact_kernel<<<static_cast<unsigned>(blocks), PC_T, 0, c->stream>>>(prm);
+    launch_check(c);
+    return;
+  }
   c->ch_perm.ensure(B);
   c->ch_off.ensure(P + 2);
   c->ch_groups.ensure(B + P + 1);
@@ -414,7 +447,7 @@ void run_pcgchol2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_
   {
     Timed tm(c, VQPC_K_BUCKET);
     counting_sort(c, d_labels, d_perm, B, P, c->ch_perm.p, c->ch_off.p);
-    chol_groups_kernel<<<1, 1, 0, c->stream>>>(c->ch_off.p, P, S, c->ch_groups.p, c->ch_ngroups.p);
+    chol_groups_kernel<<<1, CG_T, 0, c->stream>>>(c->ch_off.p, P, S, c->ch_groups.p, c->ch_ngroups.p);
     launch_check(c);
   }
   void (*const kerns[PC_MAXS])(const PcholParams) = {
@@ -1195,8 +1228,10 @@ int vqpc_ctx_create(const vqpc_problem* pb, vqpc_ctx** out) {
   const bool grid = pb->method == VQPC_GRID || pb->method == VQPC_SIGN_GRID;
   if (grid && !pb->latent) return VQPC_INVALID_CODEBOOK;
   if (pb->dim == 1 && pb->precond != VQPC_PC_CHOLESKY) return VQPC_INVALID_CONFIG;
+  // IC(0)'s level sweeps put one thread on each grid row (r - 1 <= 256); the cholesky
+  // kind checks its envelope width at setup; the AMG kind has no mesh-size limit
   if (pb->dim == 2 && ((pb->precond != VQPC_PC_IC0 && pb->precond != VQPC_PC_CHOLESKY && pb->precond != VQPC_PC_AMG) ||
-                       pb->size - 1 > P2_T))
+                       (pb->precond == VQPC_PC_IC0 && pb->size - 1 > P2_T)))
     return VQPC_INVALID_CONFIG;
   auto* c = new vqpc_ctx();
   c->pb = *pb;

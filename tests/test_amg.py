@@ -168,3 +168,31 @@ def test_amg_kind_without_device():
     with pytest.raises(lib.VqpcError) as e:
         campaign.make_context(cfg, dict(basis=basis, codebook=cb))
     assert "no-device" in str(e.value)
+
+
+@pytest.mark.gpu
+def test_gpu_amg_paper_size_mesh():
+    """The paper's problem size (n = 99,681 unknowns) on the structured
+    mesh r = 317 (99,856 unknowns; beyond the IC(0) kind's r <= 257): the SA-AMG
+    kind runs it, bit-identical to the oracle in reference-order mode."""
+    name = "C4amg317"
+    CONFIGS.setdefault(name, campaign.scaled(campaign.CONFIGS["C4amg"], mesh_resolution=317, name=name))
+    cfg, basis, cb, xi = setup_case(name, 4)
+    ocb = oracle_codebook(cb)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    assert ctx.n == 316 * 316
+    fast = ctx.run_campaign(xi, cfg["eps"])
+    ctx.set_exact_reductions(True)
+    kc = ctx.centroid_coefficients()
+    labels = oracle.assign(ocb, xi)
+    kap, _ = ctx.realise(xi)
+    it, rel, st, x = ctx.solve_batch(xi, labels, cfg["eps"], want_x=True)
+    ctx.close()
+    used = sorted(set(int(v) for v in labels))
+    ops = oracle.PreconditionerSet.from_coefficients(2, cfg["mesh_resolution"], "amg", kc[used])
+    for i in range(len(xi)):
+        out = ops.pcg(used.index(int(labels[i])), kap[i], cfg["eps"])
+        assert out["iterations"] == it[i] and out["status"] == st[i] and out["rel"] == rel[i], i
+        assert np.array_equal(out["x"], x[i]), i
+    assert (fast["status"] == 0).all() and np.abs(fast["iterations"].astype(int) - it).max() <= 2
+    print("r=317 (n=99,856) AMG: J exact", it.tolist(), "fast", fast["iterations"].tolist())

@@ -5,11 +5,21 @@ the CPU oracle's restatement (oracle/src/vqp_oracle.cpp CholeskyPreconditioner).
 * the factor is bit-identical: the GPU's serial apply (vqpc_precond_apply) equals
   the oracle's apply bit for bit, which needs the same RCM permutation, envelope
   and every factor entry;
-* the batched solve (blocked triangular solves, tree dot products) reproduces the
-  oracle's iteration counts within +-1 and its solutions to 1e-10 (relative l2),
-  for 1, 2 and 4 right-hand sides per CTA and meshes whose row count is not a
-  multiple of the 32-row block.
+* the reference-order mode (serial dots, Eigen-order triangular solves:
+  forward column-major lower, backward row-major upper view) is bit-identical to
+  the oracle: J, status, final residual and x;
+* the batched throughput solve (blocked DMMA triangular solves, tree dot
+  products) is compared with the oracle beside the oracle's own FMA build (the
+  rounding-level yardstick): statuses identical, max |dJ| and the mean-J gap no
+  larger than the yardstick's plus one iteration / 0.5 iterations, x to 1e-10
+  (relative l2) where J agrees; for 1, 2, 4 and 8 right-hand sides per CTA, on
+  meshes whose row count is not a multiple of the 32-row block, and at r = 64,
+  128, 200 and 257 (envelope width W = 256, the DMMA window's limit; the ring
+  wraps and the backward sweep reloads y blocks).
 """
+from concurrent.futures import ThreadPoolExecutor
+import os
+
 import numpy as np
 import pytest
 
@@ -41,8 +51,16 @@ def test_chol2d_factor_and_apply_bit_identical(r):
     ctx.close()
 
 
-@pytest.mark.parametrize("S", [1, 2, 4, 8])
-@pytest.mark.parametrize("r,n_real", [(32, 48), (30, 24)])
+def _oracle_solves(pset, labels, kap, eps, n_threads=None):
+    def one(i):
+        return pset.pcg(int(labels[i]), kap[i], eps)
+    with ThreadPoolExecutor(n_threads or os.cpu_count()) as ex:
+        return list(ex.map(one, range(len(labels))))
+
+
+@pytest.mark.parametrize("S,r,n_real", [(S, r, n) for S in (1, 2, 4, 8) for r, n in ((32, 48), (30, 24))]
+                         + [(2, 64, 32), (8, 64, 32), (4, 128, 16), (8, 128, 16), (8, 200, 8), (2, 257, 6),
+                            (8, 257, 8)])
 def test_chol2d_solve_parity(monkeypatch, S, r, n_real):
     monkeypatch.setenv("VQPC_CHOL_S", str(S))
     cfg, basis, cb, xi = setup_case(_cfg_name(r), n_real)
@@ -50,23 +68,47 @@ def test_chol2d_solve_parity(monkeypatch, S, r, n_real):
     kc = ctx.centroid_coefficients()
     labels = oracle.assign(oracle_codebook(cb), xi)
     kap, _ = ctx.realise(xi)
-    pset = oracle.PreconditionerSet.from_coefficients(2, r, "cholesky", kc)
     it, rel, st, x = ctx.solve_batch(xi, labels, cfg["eps"], want_x=True)
-    jc = np.empty(len(xi), dtype=np.int64)
-    dx = np.empty(len(xi))
-    for i in range(len(xi)):
-        out = pset.pcg(int(labels[i]), kap[i], cfg["eps"])
-        assert out["status"] == st[i], i
-        assert rel[i] < cfg["eps"]
-        jc[i] = out["iterations"]
-        dx[i] = np.linalg.norm(out["x"] - x[i]) / np.linalg.norm(out["x"])
-    dj = np.abs(jc - it)
-    print(f"r={r} S={S}: J gpu {it.mean():.3f} cpu {jc.mean():.3f}, |dJ| max {dj.max()} frac>0 {np.mean(dj > 0):.3f};"
-          f" rel-l2(x) max {dx.max():.2e}, on equal J {dx[dj == 0].max():.2e}")
-    assert dj.max() <= 2 and np.mean(dj > 1) <= 0.05
-    assert abs(it.mean() - jc.mean()) < 0.5
-    assert dx[dj == 0].max() < 1e-10
     ctx.close()
+    pset = oracle.PreconditionerSet.from_coefficients(2, r, "cholesky", kc)
+    outs = _oracle_solves(pset, labels, kap, cfg["eps"])
+    with oracle.fma_variant():
+        pf = oracle.PreconditionerSet.from_coefficients(2, r, "cholesky", kc)
+        outs_f = _oracle_solves(pf, labels, kap, cfg["eps"])
+    jc = np.array([o["iterations"] for o in outs])
+    jf = np.array([o["iterations"] for o in outs_f])
+    assert [o["status"] for o in outs] == list(st)
+    assert (rel < cfg["eps"]).all()
+    dx = np.array([np.linalg.norm(o["x"] - x[i]) / np.linalg.norm(o["x"]) for i, o in enumerate(outs)])
+    dj, dy = np.abs(jc - it), np.abs(jc - jf)
+    print(f"r={r} S={S}: J gpu {it.mean():.3f} cpu {jc.mean():.3f} cpu+fma {jf.mean():.3f}; |dJ| max {dj.max()} "
+          f"(fma {dy.max()}) frac>0 {np.mean(dj > 0):.3f} (fma {np.mean(dy > 0):.3f}); rel-l2(x) max {dx.max():.2e}, "
+          f"on equal J {dx[dj == 0].max() if (dj == 0).any() else 0:.2e}")
+    assert dj.max() <= dy.max() + 1
+    assert abs(it.mean() - jc.mean()) <= abs(jf.mean() - jc.mean()) + 0.5
+    if (dj == 0).any():
+        assert dx[dj == 0].max() < 1e-10
+
+
+@pytest.mark.parametrize("r,n_real", [(17, 16), (32, 24), (64, 8)])
+def test_chol2d_exact_mode_bit_identical(r, n_real):
+    """Reference-order mode of the 2-D cholesky kind (pcgchol2d_exact_kernel): with
+    the same coefficient bits, J, status, final residual and x equal the oracle's
+    (Eigen's solve order in both triangular sweeps, serial natural-order dots)."""
+    cfg, basis, cb, xi = setup_case(_cfg_name(r), n_real)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    ctx.set_exact_reductions(True)
+    kc = ctx.centroid_coefficients()
+    labels = oracle.assign(oracle_codebook(cb), xi)
+    kap, _ = ctx.realise(xi)
+    it, rel, st, x = ctx.solve_batch(xi, labels, cfg["eps"], want_x=True)
+    ctx.close()
+    pset = oracle.PreconditionerSet.from_coefficients(2, r, "cholesky", kc)
+    for i, out in enumerate(_oracle_solves(pset, labels, kap, cfg["eps"])):
+        assert out["iterations"] == it[i] and out["status"] == st[i], (i, out["iterations"], it[i])
+        assert out["rel"] == rel[i], i
+        assert np.array_equal(out["x"], x[i]), i
+    print(f"chol2d exact mode r={r}: {n_real} samples bit-identical, mean J {it.mean():.2f}")
 
 
 def test_chol2d_campaign_vs_oracle():
@@ -110,11 +152,17 @@ def test_chol2d_records_edges(monkeypatch):
     ctx.close()
 
 
-def test_chol2d_rejects_exact_mode():
-    cfg, basis, cb, xi = setup_case(_cfg_name(32), 4)
-    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
-    ctx.set_exact_reductions(True)
-    labels = oracle.assign(oracle_codebook(cb), xi)
-    with pytest.raises(lib.VqpcError, match="invalid-config"):
-        ctx.solve_batch(xi, labels, cfg["eps"])
-    ctx.close()
+def test_chol_groups_cover_every_sample(monkeypatch):
+    """The parallel group builder (chol_groups_kernel) emits every solved sample in
+    exactly one group: a campaign with skewed buckets gives the same records for
+    S = 1 and S = 8."""
+    cfg, basis, cb, xi = setup_case(_cfg_name(17), 64)
+    out = []
+    for S in ("1", "8"):  # the group size is read when the context is created
+        monkeypatch.setenv("VQPC_CHOL_S", S)
+        ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+        out.append(ctx.run_campaign(xi, cfg["eps"]))
+        ctx.close()
+    a, b = out
+    assert np.array_equal(a["labels"], b["labels"]) and np.array_equal(a["status"], b["status"])
+    assert (a["status"] == 0).all() and np.array_equal(a["n_p"], b["n_p"])
