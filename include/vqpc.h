@@ -206,6 +206,16 @@ int vqpc_run_campaign_x(vqpc_ctx* ctx, const double* xi, int64_t B, int ld, doub
                         int64_t chunk, int64_t solve_limit, int32_t* labels, int32_t* iters,
                         double* final_rel, uint8_t* status, int64_t* stats, int64_t* summary, double* x_out);
 
+/* ---- ideal sweep (driver.cpp:290-340): for every realisation i (xi: B x ld host
+ * rows, all n_kl modes lifted for the system) and every m of m_list, the
+ * preconditioner of the context's kind built from the m-truncated coefficient
+ * transport(lift(basis, xi_i[0:m])) and applied to the full-coefficient system.
+ * Records are B x n_m row-major (record of (i, m_list[j]) at i * n_m + j); the
+ * rows {m, relative energy, mean J over converged records} follow on the host.
+ * The context's centroid factors are kept (set aside during the sweep). ----- */
+int vqpc_ideal_sweep(vqpc_ctx* ctx, const double* xi, int64_t B, int ld, const int* m_list, int n_m, double eps,
+                     int max_iter, int32_t* iters, double* final_rel, uint8_t* status);
+
 /* ---- per-kernel device timing (CUDA events on the context's stream) ------
  * enable != 0 brackets every kernel launch with events; vqpc_profile_read
  * synchronises and returns, per kernel kind, the accumulated milliseconds and

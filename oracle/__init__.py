@@ -382,6 +382,20 @@ class PreconditionerSet:
         return out
 
 
+def ideal_sweep(dim, size, kind, evals, evecs, xi, m_list, eps, max_iter=-1, threads=None):
+    """driver.cpp:290-340 restated: per-(realisation, m) records (B x n_m arrays)."""
+    evals, evecs, xi = f64(evals), f64(evecs), f64(np.atleast_2d(xi))
+    B, ld = xi.shape
+    ml = np.ascontiguousarray(m_list, dtype=np.int32)
+    it = np.empty((B, ml.size), np.int32)
+    rel = np.empty((B, ml.size))
+    st = np.empty((B, ml.size), np.uint8)
+    _check(lib().vqpo_ideal_sweep(I(dim), I(size), I(PRECONDS[kind]), _p(evals), _p(evecs), I(evecs.shape[0]),
+                                  I(evecs.shape[1]), _p(xi), I64(B), I(ld), _p(ml), I(ml.size), D(eps), I(max_iter),
+                                  I(threads or os.cpu_count() or 1), _p(it), _p(rel), _p(st)))
+    return dict(iterations=it, rel=rel, status=st)
+
+
 def run_campaign(dim, size, kind, cb: Codebook, evals, evecs, xi, eps, max_iter=-1, threads=None):
     """driver.cpp:193-281 restated: returns per-sample arrays, per-centroid stats
     and stage timings (seconds)."""

@@ -1482,6 +1482,47 @@ int vqpo_pcg_coefficient(void* h, int p, const double* kappa, double eps, int ma
 // stats (length 4P): [n_p | sum_j | conv_count | conv_sum]; summary[0..3] =
 // {total_iterations, unconverged, conv_total, conv_sum_total};
 // timings[0..3] = seconds {assign, build, solve, reduce}.
+// ideal_sweep (driver.cpp:290-340): for every realisation i (threads over
+// realisations, driver.cpp:313) and every m of m_list, the preconditioner of the
+// kind built from the m-truncated coefficient transport(lift(basis, xi_i[0:m]))
+// applied to the full-coefficient system; records[i * n_m + im]. The rows
+// (m, relative energy, mean J over converged) are formed by the caller.
+int vqpo_ideal_sweep(int dim, int size, int kind, const double* evals, const double* evecs, int n_kl, int n_nodes,
+                     const double* xi, int64_t B, int ld, const int* m_list, int n_m, double eps, int max_iter,
+                     int threads, int32_t* iters, double* rel, uint8_t* status) {
+  VQPO_GUARD({
+    if (!(eps > 0.0) || eps >= 1.0) throw Err(INVALID_TOLERANCE);
+    Model model{dim, size};
+    if (model.n_nodes() != n_nodes || ld < n_kl) throw Err(INVALID_CONFIG);
+    for (int im = 0; im < n_m; ++im)
+      if (m_list[im] < 0 || m_list[im] > n_kl) throw Err(MODE_COUNT_OUT_OF_RANGE);
+    parallel_for_slots(static_cast<long>(B), threads, [&](long i) {
+      const double* xr = xi + static_cast<size_t>(i) * ld;
+      std::vector<double> h(n_nodes), ht(n_nodes);
+      for (int im = 0; im < n_m; ++im) {
+        Record rec;
+        try {
+          lift(evals, evecs, n_nodes, xr, n_kl, h.data());
+          transport(h.data(), n_nodes);
+          const System sys = model.assemble(h.data());
+          lift(evals, evecs, n_nodes, xr, m_list[im], ht.data());
+          transport(ht.data(), n_nodes);
+          const System trunc = model.assemble(ht.data());
+          const auto M = build_preconditioner(kind, model, trunc.A);
+          rec = pcg(sys, *M, eps, max_iter, nullptr, nullptr);
+        } catch (const Err& e) {
+          rec = Record{};
+          rec.status = e.code == COEFFICIENT_OVERFLOW ? ST_COEFF_OVERFLOW : ST_INVALID_COEFF;
+        }
+        const size_t q = static_cast<size_t>(i) * n_m + im;
+        iters[q] = rec.iterations;
+        rel[q] = rec.rel;
+        status[q] = rec.status;
+      }
+    });
+  })
+}
+
 int vqpo_run_campaign(int dim, int size, int kind, int method, int map, int P, int m,
                       const double* lambdas, const double* centroids, const double* latent,
                       const double* evals, const double* evecs, int n_kl, int n_nodes, const double* xi,

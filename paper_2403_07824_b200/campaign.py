@@ -215,3 +215,37 @@ def run_campaign_with(cfg, artifacts, xi, ctx=None, chunk=None):
             ctx.close()
     res["report"] = report_from(res, artifacts["codebook"])
     return res
+
+
+def relative_energy(basis, m):
+    """relative_energy (field.cpp:87-93): 1 - truncation_error(m) / total_variance."""
+    tv = float(basis["total_variance"])
+    return 1.0 - (tv - float(np.sum(basis["eigenvalues"][:m]))) / tv
+
+
+def sweep_rows(basis, m_list, records):
+    """SweepRow{m, relative_energy, mean_j} per m (driver.cpp:325-338): mean J over
+    the converged records of that m."""
+    rows = []
+    for j, m in enumerate(m_list):
+        conv = records["status"][:, j] == 0
+        its = records["iterations"][:, j][conv].astype(np.int64)
+        rows.append(dict(m=int(m), relative_energy=relative_energy(basis, int(m)),
+                         mean_j=float(its.sum()) / conv.sum() if conv.any() else 0.0))
+    return rows
+
+
+def ideal_sweep(cfg, artifacts, xi, m_list, ctx=None):
+    """ideal_sweep (driver.cpp:290-340) on the GPU: per-realisation preconditioners
+    from the m-truncated coefficients, applied to the full-coefficient systems.
+    Returns the records (B x len(m_list)) and the reference's SweepRow list."""
+    own = ctx is None
+    if own:
+        ctx = make_context(cfg, artifacts, factor=False)
+    try:
+        rec = ctx.ideal_sweep(xi, m_list, cfg["eps"])
+    finally:
+        if own:
+            ctx.close()
+    rec["rows"] = sweep_rows(artifacts["basis"], m_list, rec)
+    return rec

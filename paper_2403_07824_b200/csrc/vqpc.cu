@@ -591,7 +591,9 @@ void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d
   prm.gmap = c->gmap.p;
   if (!c->b2_checked) {  // is b_i = area_sum_i / 3 the same for every node? (yes when h = 1/r is exact)
     c->bvec2.ensure(c->n);
-    build_bvec_kernel<<<64, P2_T, 0, c->stream>>>(c->g2, c->kappa_c.p, c->gmap.p, c->bvec2.p);
+    // b does not depend on kappa; any coefficient row serves the assembly call
+    build_bvec_kernel<<<64, P2_T, 0, c->stream>>>(c->g2, c->kappa_c.p ? c->kappa_c.p : d_kappa, c->gmap.p,
+                                                  c->bvec2.p);
     launch_check(c);
     std::vector<double> hb(c->n);
     CK(cudaMemcpyAsync(hb.data(), c->bvec2.p, sizeof(double) * c->n, cudaMemcpyDeviceToHost, c->stream));
@@ -775,6 +777,12 @@ __global__ void stats_kernel(const int32_t* labels, const int32_t* iters, const 
   }
 }
 
+__global__ void iota_kernel(int32_t* v, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    v[i] = static_cast<int32_t>(i);
+}
+
 __global__ void mark_unsolved_kernel(int32_t* iters, double* rel, uint8_t* status, int64_t B) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= B) return;
@@ -935,11 +943,11 @@ void setup_chol2d(vqpc_ctx* c) {
 // the oracle's operations (amg_centroid_rows_kernel), the P hierarchies are built on
 // host threads (amg_setup.cuh; independent per centroid, as the reference builds
 // each AmgPreconditioner, driver.cpp:212-219) and packed as sliced ELL.
-void setup_amg(vqpc_ctx* c, int64_t ldk) {
-  const int P = c->pb.P, n = c->n;
+void setup_amg(vqpc_ctx* c, const double* d_kc, int64_t ldk, int P) {
+  const int n = c->n;
   DBuf<double> rows;
   rows.ensure(static_cast<size_t>(P) * n * 7);
-  amg_centroid_rows_kernel<<<4 * c->sm_count, 256, 0, c->stream>>>(c->kappa_c.p, ldk, P, c->g2, rows.p);
+  amg_centroid_rows_kernel<<<4 * c->sm_count, 256, 0, c->stream>>>(d_kc, ldk, P, c->g2, rows.p);
   launch_check(c);
   std::vector<double> hv(static_cast<size_t>(P) * n * 7);
   d2h(c, hv.data(), rows.p, hv.size());
@@ -1068,6 +1076,50 @@ void setup_amg(vqpc_ctx* c, int64_t ldk) {
   CK(cudaStreamSynchronize(c->stream));
   c->amg_cv = (cv_max + 1) & ~1;
   c->amg_entries = entries / P;
+}
+
+// Factor P coefficient fields (d_kc: P rows of ldk nodal/elemental values) into the
+// context's factor buffers, indexed by label 0..P-1: the per-centroid step of
+// run_campaign_with (driver.cpp:212-219), also used by the ideal sweep with one
+// factor per realisation (driver.cpp:317-320). Throws not-spd.
+void factor_coefficients(vqpc_ctx* c, const double* d_kc, int64_t ldk, int P) {
+  const vqpc_problem& pb = c->pb;
+    c->err.ensure(1);
+    CK(cudaMemsetAsync(c->err.p, 0, sizeof(int), c->stream));
+    if (pb.dim == 2 && c->chol2d) {
+      c->ch_L.ensure(static_cast<size_t>(P) * c->ch_ldL);
+      c->ch_Linv.ensure(static_cast<size_t>(P) * c->ch_ldLi);
+      Timed tm(c, VQPC_K_OTHER);
+      cholfactor2d_kernel<<<P, PC_T, 0, c->stream>>>(d_kc, ldk, P, c->g2, c->clay, c->ch_L.p, c->ch_ldL,
+                                                     c->err.p);
+      launch_check(c);
+      const int64_t th = static_cast<int64_t>(P) * c->clay.nblk * PC_BS;
+      cholinv_kernel<<<static_cast<unsigned>(ceil_div(th, 128)), 128, 0, c->stream>>>(c->ch_L.p, c->ch_ldL, c->clay,
+                                                                                      P, c->ch_Linv.p, c->ch_ldLi);
+      launch_check(c);
+      for (int p = 0; p < P; ++p)  // each block record's metadata tail (one TMA copy per block)
+        CK(cudaMemcpy2DAsync(c->ch_Linv.p + static_cast<size_t>(p) * c->ch_ldLi + PC_STG_META, PC_LIB * sizeof(double),
+                             c->ch_bmeta.p, 2 * PC_BS * sizeof(int), 2 * PC_BS * sizeof(int), c->clay.nblk,
+                             cudaMemcpyDeviceToDevice, c->stream));
+    } else if (pb.dim == 2 && c->amg) {
+      setup_amg(c, d_kc, ldk, P);
+    } else if (pb.dim == 2) {
+      c->fac2.ensure(static_cast<size_t>(P) * P2_FAC * c->n);
+      Timed tm(c, VQPC_K_OTHER);
+      factor2d_kernel<<<P, P2_T, 0, c->stream>>>(d_kc, ldk, P, c->g2, c->fac2.p, c->err.p);
+      launch_check(c);
+    } else {
+      c->fac.ensure(static_cast<size_t>(P) * c->NP);
+      Timed tm(c, VQPC_K_OTHER);
+      factor1d_kernel<<<static_cast<unsigned>(ceil_div(P, 64)), 64, 0, c->stream>>>(d_kc, ldk, P, c->n,
+                                                                                      h_of(pb), c->fac.p, c->NP,
+                                                                                      c->err.p);
+      launch_check(c);
+    }
+  int err = 0;
+  d2h(c, &err, c->err.p, 1);
+  CK(cudaStreamSynchronize(c->stream));
+  if (err) throw ApiError{VQPC_NOT_SPD, "not-spd"};
 }
 
 // The full campaign on device-resident arrays (run_campaign_with semantics).
@@ -1385,38 +1437,7 @@ int vqpc_factor_centroids(vqpc_ctx* c) {
     c->kflag.ensure(static_cast<size_t>(P) + 4);  // + 4: word-wide atomicOr flags
     CK(cudaMemsetAsync(c->kflag.p, 0, P, c->stream));
     run_realise(c, c->xi.p, P, std::max(m, 1), m, c->kappa_c.p, ldk, c->kflag.p);
-    c->err.ensure(1);
-    CK(cudaMemsetAsync(c->err.p, 0, sizeof(int), c->stream));
-    if (pb.dim == 2 && c->chol2d) {
-      c->ch_L.ensure(static_cast<size_t>(P) * c->ch_ldL);
-      c->ch_Linv.ensure(static_cast<size_t>(P) * c->ch_ldLi);
-      Timed tm(c, VQPC_K_OTHER);
-      cholfactor2d_kernel<<<P, PC_T, 0, c->stream>>>(c->kappa_c.p, ldk, P, c->g2, c->clay, c->ch_L.p, c->ch_ldL,
-                                                     c->err.p);
-      launch_check(c);
-      const int64_t th = static_cast<int64_t>(P) * c->clay.nblk * PC_BS;
-      cholinv_kernel<<<static_cast<unsigned>(ceil_div(th, 128)), 128, 0, c->stream>>>(c->ch_L.p, c->ch_ldL, c->clay,
-                                                                                      P, c->ch_Linv.p, c->ch_ldLi);
-      launch_check(c);
-      for (int p = 0; p < P; ++p)  // each block record's metadata tail (one TMA copy per block)
-        CK(cudaMemcpy2DAsync(c->ch_Linv.p + static_cast<size_t>(p) * c->ch_ldLi + PC_STG_META, PC_LIB * sizeof(double),
-                             c->ch_bmeta.p, 2 * PC_BS * sizeof(int), 2 * PC_BS * sizeof(int), c->clay.nblk,
-                             cudaMemcpyDeviceToDevice, c->stream));
-    } else if (pb.dim == 2 && c->amg) {
-      setup_amg(c, ldk);
-    } else if (pb.dim == 2) {
-      c->fac2.ensure(static_cast<size_t>(P) * P2_FAC * c->n);
-      Timed tm(c, VQPC_K_OTHER);
-      factor2d_kernel<<<P, P2_T, 0, c->stream>>>(c->kappa_c.p, ldk, P, c->g2, c->fac2.p, c->err.p);
-      launch_check(c);
-    } else {
-      c->fac.ensure(static_cast<size_t>(P) * c->NP);
-      Timed tm(c, VQPC_K_OTHER);
-      factor1d_kernel<<<static_cast<unsigned>(ceil_div(P, 64)), 64, 0, c->stream>>>(c->kappa_c.p, ldk, P, c->n,
-                                                                                      h_of(pb), c->fac.p, c->NP,
-                                                                                      c->err.p);
-      launch_check(c);
-    }
+    factor_coefficients(c, c->kappa_c.p, ldk, P);
     int err = 0;
     std::vector<uint8_t> flags(P);
     d2h(c, &err, c->err.p, 1);
@@ -1718,6 +1739,114 @@ int vqpc_run_campaign_x(vqpc_ctx* c, const double* xi, int64_t B, int ld, double
     d2h(c, summary, c->stats.p + 4 * P, 4);
     d2h(c, x_out, c->x.p, static_cast<size_t>(B) * c->n);
     CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+// ideal_sweep (driver.cpp:290-340) on the device: for every m of m_list, the
+// realisations are taken in chunks; each chunk's m-truncated coefficients are
+// realised and factored as if they were centroids (one preconditioner per
+// realisation, label i -> factor i), and the chunk's full-coefficient systems are
+// solved with them by the campaign's own PCG kernels. The context's centroid
+// factors are set aside for the sweep and restored after it.
+int vqpc_ideal_sweep(vqpc_ctx* c, const double* xi, int64_t B, int ld, const int* m_list, int n_m, double eps,
+                     int max_iter, int32_t* iters, double* final_rel, uint8_t* status) {
+  if (!c || (B > 0 && (!xi || !iters || !final_rel || !status)) || n_m < 0 || (n_m > 0 && !m_list))
+    return VQPC_INVALID_ARGUMENT;
+  return guard(c, [&] {
+    if (!(eps > 0.0) || eps >= 1.0) throw ApiError{VQPC_INVALID_TOLERANCE, "invalid-tolerance"};
+    if (ld < c->pb.n_kl) throw ApiError{VQPC_INVALID_ARGUMENT, "ld < n_kl"};
+    for (int im = 0; im < n_m; ++im)
+      if (m_list[im] < 0 || m_list[im] > c->pb.n_kl)
+        throw ApiError{VQPC_MODE_COUNT_OUT_OF_RANGE, "mode-count-out-of-range"};
+    if (B <= 0 || n_m == 0) return;
+    const int64_t ldk = kappa_ld(c);
+    c->xi.ensure(static_cast<size_t>(B) * ld);
+    h2d(c, c->xi.p, xi, static_cast<size_t>(B) * ld);
+    c->kappa.ensure(static_cast<size_t>(B) * ldk);
+    c->kflag.ensure(static_cast<size_t>(B) + 4);
+    CK(cudaMemsetAsync(c->kflag.p, 0, B, c->stream));
+    run_realise(c, c->xi.p, B, ld, c->pb.n_kl, c->kappa.p, ldk, c->kflag.p);
+    // per-realisation factors: how many fit at once (1-D 2n doubles each; 2-D IC(0) 4n;
+    // cholesky nnz(L); AMG a hierarchy built on the host)
+    // (the cholesky kind's group builder buckets labels into pb.P bins: at most P per chunk)
+    const int64_t nc = std::min<int64_t>(B, c->pb.dim == 1 ? 8192
+                                            : c->chol2d  ? std::min(32, c->pb.P)
+                                            : c->amg     ? 256
+                                                         : 1024);
+    DBuf<double> kc;
+    DBuf<uint8_t> kcf;
+    DBuf<int32_t> ids, d_it;
+    DBuf<double> d_rel;
+    DBuf<uint8_t> d_st;
+    kc.ensure(static_cast<size_t>(nc) * ldk);
+    kcf.ensure(static_cast<size_t>(nc) + 4);
+    ids.ensure(nc);
+    d_it.ensure(B);
+    d_rel.ensure(B);
+    d_st.ensure(B);
+    iota_kernel<<<static_cast<unsigned>(ceil_div(nc, 256)), 256, 0, c->stream>>>(ids.p, nc);
+    launch_check(c);
+    // set the centroid factors aside
+    auto swap_factors = [&](vqpc_ctx& o) {
+      std::swap(c->fac, o.fac);
+      std::swap(c->fac2, o.fac2);
+      std::swap(c->ch_L, o.ch_L);
+      std::swap(c->ch_Linv, o.ch_Linv);
+      std::swap(c->amg_i, o.amg_i);
+      std::swap(c->amg_d, o.amg_d);
+      std::swap(c->amg_hd, o.amg_hd);
+      std::swap(c->amg_h, o.amg_h);
+      std::swap(c->amg_cv, o.amg_cv);
+      std::swap(c->amg_entries, o.amg_entries);
+      std::swap(c->fac_lu, o.fac_lu);
+      std::swap(c->have_lu, o.have_lu);
+    };
+    vqpc_ctx saved;
+    swap_factors(saved);
+    auto release = [&](vqpc_ctx& o) {
+      for (auto* b : {&o.fac2, &o.ch_L, &o.ch_Linv, &o.amg_d}) b->release();
+      o.fac.release();
+      o.fac_lu.release();
+      o.amg_i.release();
+      o.amg_hd.release();
+    };
+    std::vector<int32_t> h_it(B);
+    std::vector<double> h_rel(B);
+    std::vector<uint8_t> h_st(B);
+    try {
+      for (int im = 0; im < n_m; ++im) {
+        for (int64_t c0 = 0; c0 < B; c0 += nc) {
+          const int64_t nb = std::min(nc, B - c0);
+          CK(cudaMemsetAsync(kcf.p, 0, nb, c->stream));
+          run_realise(c, c->xi.p + c0 * ld, nb, ld, m_list[im], kc.p, ldk, kcf.p);
+          std::vector<uint8_t> f(nb);
+          d2h(c, f.data(), kcf.p, nb);
+          CK(cudaStreamSynchronize(c->stream));
+          for (uint8_t v : f)
+            if (v) throw ApiError{v & 1 ? VQPC_COEFFICIENT_OVERFLOW : VQPC_INVALID_COEFFICIENT,
+                                  "truncated coefficient of the ideal sweep is not finite / positive"};
+          c->have_lu = false;
+          factor_coefficients(c, kc.p, ldk, static_cast<int>(nb));
+          run_pcg(c, c->kappa.p + c0 * ldk, ldk, c->kflag.p + c0, ids.p, ids.p, nb, c0, eps, max_iter, nullptr,
+                  d_it.p, d_rel.p, d_st.p, nullptr);
+        }
+        d2h(c, h_it.data(), d_it.p, B);
+        d2h(c, h_rel.data(), d_rel.p, B);
+        d2h(c, h_st.data(), d_st.p, B);
+        CK(cudaStreamSynchronize(c->stream));
+        for (int64_t i = 0; i < B; ++i) {
+          iters[i * n_m + im] = h_it[i];
+          final_rel[i * n_m + im] = h_rel[i];
+          status[i * n_m + im] = h_st[i];
+        }
+      }
+    } catch (...) {
+      release(*c);
+      swap_factors(saved);
+      throw;
+    }
+    release(*c);
+    swap_factors(saved);
   });
 }
 

@@ -79,6 +79,7 @@ def load():
             "vqpc_debug_pcg1d_phase_cycles": (I, [C.POINTER(C.c_ulonglong), I]),
             "vqpc_counter_hash": (U64, [U64, U64, U64]),
             "vqpc_amg_info": (I, [VP, I, I, VP, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+            "vqpc_ideal_sweep": (I, [VP, VP, I64, I, VP, I, D, I, VP, VP, VP]),
             "vqpc_amg_level": (I, [VP, I, I, VP, VP, VP, VP, VP, VP, VP, VP]),
             "vqpc_normal_quantile": (D, [D]),
         }
@@ -234,6 +235,18 @@ class Context:
         self._c(load().vqpc_factor_centroids(self.h))
         self.factored = True
         self.factor_entries = int(load().vqpc_factor_entries(self.h))
+
+    def ideal_sweep(self, xi, m_list, eps, max_iter=-1):
+        """ideal_sweep records (driver.cpp:290-340): B x len(m_list) arrays."""
+        xi = f64(np.atleast_2d(xi))
+        B, ld = xi.shape
+        ml = np.ascontiguousarray(m_list, dtype=np.int32)
+        it = np.empty((B, ml.size), np.int32)
+        rel = np.empty((B, ml.size))
+        st = np.empty((B, ml.size), np.uint8)
+        self._c(load().vqpc_ideal_sweep(self.h, _p(xi), B, ld, _p(ml), ml.size, eps, max_iter, _p(it), _p(rel),
+                                        _p(st)))
+        return dict(iterations=it, rel=rel, status=st)
 
     def amg_levels(self, p):
         """SA-AMG hierarchy of centroid p as built by the library (same layout as
