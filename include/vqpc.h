@@ -246,6 +246,18 @@ int vqpc_kmeans(int device, const double* samples, int n, int m, const double* l
                 uint64_t init_seed, int max_iter, double rel_tol, double* centroids_out,
                 double* history_out, int* n_history);
 
+/* ---- KL basis on the device: build_kl_basis (field.cpp:22-82) by Lanczos with
+ * full reorthogonalisation on the lumped-Galerkin operator W = M^1/2 C M^1/2,
+ * applied matrix-free (1-D: element midpoints, weights h; 2-D: the structured
+ * (size+1)^2 node grid with the Kronecker factorisation of the squared-exponential
+ * kernel). Keeps the n_kl dominant modes above the reference's degeneracy cutoff
+ * 1e-12 lambda_1 (cutoff != 0; else all positive ones), Phi = v / sqrt(mass),
+ * first entry of largest magnitude positive. Outputs: eigenvalues (n_kl,
+ * descending), eigenvectors (n_kl x n_nodes, mode-major), mass (n_nodes,
+ * nullable); *kept = modes kept. */
+int vqpc_kl_basis(int device, int dim, int size, double sigma2, double ell, int n_kl, int cutoff,
+                  double* eigenvalues_out, double* eigenvectors_out, double* mass_out, int* kept);
+
 /* ---- coefficient sampling (rng.hpp:14-31, rng.cpp:7-12) on the host -------
  * out[i*m+k] = gaussian_draw(seed, index0 + i, k). */
 int vqpc_draw_standard_normal(int64_t n, int m, uint64_t seed, int64_t index0, double* out, int threads);

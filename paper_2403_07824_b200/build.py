@@ -15,8 +15,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.environ.get("VQPC_LIB", os.path.join(HERE, "libvqpc.so"))
-SOURCES = ["vqpc.cu", "host_quantizer.cu"]
-HEADERS = ["common.cuh", "realise.cuh", "assign.cuh", "bucket.cuh", "factor.cuh", "pcg1d.cuh", "pcg1d_exact.cuh", "pcg2d.cuh", "pcgchol2d.cuh"]
+SOURCES = ["vqpc.cu", "host_quantizer.cu", "klbasis.cu"]
+HEADERS = ["amg_setup.cuh", "pcgamg2d.cuh", "common.cuh", "realise.cuh", "assign.cuh", "bucket.cuh", "factor.cuh", "pcg1d.cuh", "pcg1d_exact.cuh", "pcg2d.cuh", "pcgchol2d.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 EXTRA = os.environ.get("VQPC_NVCC_FLAGS", "").split()
@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             sys.stderr.write(r.stderr)
         objs.append(o)
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lpthread"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lpthread", "-lcublas"]
     subprocess.check_call(cmd)
     return LIB
 

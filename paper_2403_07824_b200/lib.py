@@ -80,6 +80,7 @@ def load():
             "vqpc_counter_hash": (U64, [U64, U64, U64]),
             "vqpc_amg_info": (I, [VP, I, I, VP, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
             "vqpc_ideal_sweep": (I, [VP, VP, I64, I, VP, I, D, I, VP, VP, VP]),
+            "vqpc_kl_basis": (I, [I, I, I, D, D, I, I, VP, VP, VP, C.POINTER(C.c_int)]),
             "vqpc_amg_level": (I, [VP, I, I, VP, VP, VP, VP, VP, VP, VP, VP]),
             "vqpc_normal_quantile": (D, [D]),
         }
@@ -167,6 +168,21 @@ def kmeans(samples, lambdas, P, map="scale", init_seed=1, max_iter=200, rel_tol=
 
 
 # ---------------------------------------------------------------------- context
+def kl_basis(dim, size, sigma2, ell, n_kl, cutoff=True, device=0):
+    """build_kl_basis (field.cpp:22-82) on the device (Lanczos, matrix-free
+    operator): dict(eigenvalues, eigenvectors (K x N), mass, total_variance)."""
+    nn = size if dim == 1 else (size + 1) ** 2
+    lam = np.empty(n_kl)
+    phi = np.empty((n_kl, nn))
+    mass = np.empty(nn)
+    kept = C.c_int()
+    _check(load().vqpc_kl_basis(device, dim, size, sigma2, ell, n_kl, 1 if cutoff else 0, _p(lam), _p(phi),
+                                _p(mass), C.byref(kept)))
+    k = kept.value
+    return dict(eigenvalues=lam[:k].copy(), eigenvectors=np.ascontiguousarray(phi[:k]), mass=mass,
+                total_variance=sigma2 * float(mass.sum()), sigma2=sigma2, ell=ell, mesh_resolution=size, dim=dim)
+
+
 class Context:
     """One device context: basis, codebook and (after factor_centroids) the P
     centroid factors resident in HBM. Mirrors CampaignArtifacts + the P
