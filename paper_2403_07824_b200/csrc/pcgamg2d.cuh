@@ -22,6 +22,7 @@
 #pragma once
 #include "common.cuh"
 #include "pcg2d.cuh"
+#include "pcgchol2d.cuh"
 
 namespace vqpc {
 
@@ -70,17 +71,24 @@ __device__ __forceinline__ double ell_dot(const AmgEll& M, int i, const double* 
   return s;
 }
 
-// ---- one V-cycle z = M^{-1} r on hierarchy H (amg.cpp:210-225), block-wide ---------
-// Level 0: r0 (input, n0), x0 and res0 scratch, z (output). Levels >= 1 in cv
-// (per CTA). Returns this thread's r.z partial (fast mode); in exact mode the
-// products r_i z_i are stored at prod[i].
-__device__ double amg_vcycle(const AmgHierD& H, double omega, const double* r0, double* x0, double* res0, double* z,
-                             double* cv, double* sdense, bool exact, double* prod) {
+// ---- one V-cycle z = M^{-1} r for S right-hand sides on hierarchy H ---------------
+// (amg.cpp:210-225), block-wide. Vectors hold the S slots interleaved per row
+// (v[i * S + s]): every ELL entry of the centroid's hierarchy is loaded once and
+// applied to S samples, and each gather of a neighbour row brings all S slots in
+// one sector. Level 0: r0 (input), x0 / res0 scratch, z (output); levels >= 1 in cv.
+// rz[s] accumulates this thread's r.z partial of slot s (fast mode); in exact mode
+// the products are stored at prod[s * n0 + i].
+template <int S>
+__device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, double* x0, double* res0, double* z,
+                           double* cv, double* sdense, bool exact, double* prod, double (&rz)[S]) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  auto vr = [&](int l) -> double* { return l == 0 ? const_cast<double*>(r0) : cv + H.lv[l].voff; };
-  auto vx = [&](int l) -> double* { return l == 0 ? x0 : cv + H.lv[l].voff + H.lv[l].n; };
-  auto vo = [&](int l) -> double* { return l == 0 ? res0 : cv + H.lv[l].voff + 2 * H.lv[l].n; };
+  auto vr = [&](int l) -> double* { return l == 0 ? const_cast<double*>(r0) : cv + static_cast<size_t>(H.lv[l].voff) * S; };
+  auto vx = [&](int l) -> double* { return l == 0 ? x0 : cv + (static_cast<size_t>(H.lv[l].voff) + H.lv[l].n) * S; };
+  auto vo = [&](int l) -> double* { return l == 0 ? res0 : cv + (static_cast<size_t>(H.lv[l].voff) + 2 * H.lv[l].n) * S; };
   const int last = H.nlev - 1;
+  const int n0 = H.lv[0].n;
+#pragma unroll
+  for (int s = 0; s < S; ++s) rz[s] = 0.0;
   // ---- down: pre-smooth from zero, residual, restriction -------------------------
   for (int l = 0; l < last; ++l) {
     const AmgLevelD& L = H.lv[l];
@@ -88,23 +96,45 @@ __device__ double amg_vcycle(const AmgHierD& H, double omega, const double* r0, 
     double* x = vx(l);
     double* res = vo(l);  // the residual; later this level's output
     for (int i = t; i < L.n; i += AMG_T) {
-      const double xi = __dmul_rn(omega, __dmul_rn(__ldg(L.inv_diag + i), r[i]));
-      x[i] = xi;
-      // res = r; res -= A x (Eigen's rewrite of `r - A x`), x_j recomputed with its owner's operations
+      const double di = __ldg(L.inv_diag + i);
+      double acc[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        acc[s] = r[i * S + s];
+        x[i * S + s] = __dmul_rn(omega, __dmul_rn(di, acc[s]));
+      }
+      // res = r; res -= A x (Eigen's rewrite of `r - A x`), x_c recomputed with its owner's operations
       int w;
       int e = ell_row(L.A, i, w);
-      double s = r[i];
       for (int k = 0; k < w; ++k, e += 32) {
         const int c = __ldg(L.A.col + e);
         if (c < 0) break;
-        const double xc = __dmul_rn(omega, __dmul_rn(__ldg(L.inv_diag + c), r[c]));
-        s = __dsub_rn(s, __dmul_rn(__ldg(L.A.val + e), xc));
+        const double a = __ldg(L.A.val + e), dc = __ldg(L.inv_diag + c);
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+          acc[s] = __dsub_rn(acc[s], __dmul_rn(a, __dmul_rn(omega, __dmul_rn(dc, r[c * S + s]))));
       }
-      res[i] = s;
+#pragma unroll
+      for (int s = 0; s < S; ++s) res[i * S + s] = acc[s];
     }
     __syncthreads();
     double* rn = vr(l + 1);
-    for (int c = t; c < L.nc; c += AMG_T) rn[c] = ell_dot(L.Pt, c, res);
+    for (int c = t; c < L.nc; c += AMG_T) {  // P^T residual: 0 + sum, ascending fine rows
+      double acc[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) acc[s] = 0.0;
+      int w;
+      int e = ell_row(L.Pt, c, w);
+      for (int k = 0; k < w; ++k, e += 32) {
+        const int q = __ldg(L.Pt.col + e);
+        if (q < 0) break;
+        const double v = __ldg(L.Pt.val + e);
+#pragma unroll
+        for (int s = 0; s < S; ++s) acc[s] = __dadd_rn(acc[s], __dmul_rn(v, res[q * S + s]));
+      }
+#pragma unroll
+      for (int s = 0; s < S; ++s) rn[c * S + s] = acc[s];
+    }
     __syncthreads();
   }
   // ---- coarsest ----------------------------------------------------------------
@@ -114,77 +144,134 @@ __device__ double amg_vcycle(const AmgHierD& H, double omega, const double* r0, 
     double* o = last == 0 ? z : vo(last);
     if (H.dense_n > 0) {
       const int nc = H.dense_n;
-      if (warp == 0) {
-        for (int i = lane; i < nc; i += 32) sdense[i] = r[i];
+      if (warp == 0) {  // column-oriented substitutions, S right-hand sides, rows dealt to lanes
+        for (int q = lane; q < nc * S; q += 32) sdense[q] = r[q];
         __syncwarp();
-        for (int k = 0; k < nc; ++k) {  // L y = r, column-oriented
-          if (lane == (k & 31)) sdense[k] = __ddiv_rn(sdense[k], __ldg(H.L + static_cast<size_t>(k) * nc + k));
+        for (int k = 0; k < nc; ++k) {  // L y = r
+          const double lkk = __ldg(H.L + static_cast<size_t>(k) * nc + k);
+          if (lane < S) sdense[k * S + lane] = __ddiv_rn(sdense[k * S + lane], lkk);
           __syncwarp();
-          const double yk = sdense[k];
-          for (int i = lane; i < nc; i += 32)
-            if (i > k) sdense[i] = __dsub_rn(sdense[i], __dmul_rn(__ldg(H.L + static_cast<size_t>(i) * nc + k), yk));
-          __syncwarp();
-        }
-        for (int k = nc - 1; k >= 0; --k) {  // L^T x = y, column-oriented
-          if (lane == (k & 31)) sdense[k] = __ddiv_rn(sdense[k], __ldg(H.L + static_cast<size_t>(k) * nc + k));
-          __syncwarp();
-          const double xk = sdense[k];
-          for (int i = lane; i < k; i += 32)
-            sdense[i] = __dsub_rn(sdense[i], __dmul_rn(__ldg(H.L + static_cast<size_t>(k) * nc + i), xk));
+          double yk[S];
+#pragma unroll
+          for (int s = 0; s < S; ++s) yk[s] = sdense[k * S + s];
+          for (int i = k + 1 + lane; i < nc; i += 32) {
+            const double lik = __ldg(H.L + static_cast<size_t>(i) * nc + k);
+#pragma unroll
+            for (int s = 0; s < S; ++s) sdense[i * S + s] = __dsub_rn(sdense[i * S + s], __dmul_rn(lik, yk[s]));
+          }
           __syncwarp();
         }
-        for (int i = lane; i < nc; i += 32) o[i] = sdense[i];
+        for (int k = nc - 1; k >= 0; --k) {  // L^T x = y
+          const double lkk = __ldg(H.L + static_cast<size_t>(k) * nc + k);
+          if (lane < S) sdense[k * S + lane] = __ddiv_rn(sdense[k * S + lane], lkk);
+          __syncwarp();
+          double xk[S];
+#pragma unroll
+          for (int s = 0; s < S; ++s) xk[s] = sdense[k * S + s];
+          for (int i = lane; i < k; i += 32) {
+            const double lki = __ldg(H.L + static_cast<size_t>(k) * nc + i);
+#pragma unroll
+            for (int s = 0; s < S; ++s) sdense[i * S + s] = __dsub_rn(sdense[i * S + s], __dmul_rn(lki, xk[s]));
+          }
+          __syncwarp();
+        }
+        for (int q = lane; q < nc * S; q += 32) o[q] = sdense[q];
       }
     } else {  // smoother-only bottom (amg.cpp:214-217)
       double* x = vx(last);
-      for (int i = t; i < L.n; i += AMG_T) x[i] = __dmul_rn(omega, __dmul_rn(__ldg(L.inv_diag + i), r[i]));
+      for (int i = t; i < L.n; i += AMG_T) {
+        const double di = __ldg(L.inv_diag + i);
+#pragma unroll
+        for (int s = 0; s < S; ++s) x[i * S + s] = __dmul_rn(omega, __dmul_rn(di, r[i * S + s]));
+      }
       __syncthreads();
       for (int i = t; i < L.n; i += AMG_T) {
-        const double ti = ell_dot(L.A, i, x);
-        o[i] = __dadd_rn(x[i], __dmul_rn(omega, __dmul_rn(__ldg(L.inv_diag + i), __dsub_rn(r[i], ti))));
+        double acc[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) acc[s] = 0.0;
+        int w;
+        int e = ell_row(L.A, i, w);
+        for (int k = 0; k < w; ++k, e += 32) {
+          const int c = __ldg(L.A.col + e);
+          if (c < 0) break;
+          const double a = __ldg(L.A.val + e);
+#pragma unroll
+          for (int s = 0; s < S; ++s) acc[s] = __dadd_rn(acc[s], __dmul_rn(a, x[c * S + s]));
+        }
+        const double di = __ldg(L.inv_diag + i);
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const double oi = __dadd_rn(x[i * S + s], __dmul_rn(omega, __dmul_rn(di, __dsub_rn(r[i * S + s], acc[s]))));
+          o[i * S + s] = oi;
+          if (last == 0) {
+            rz[s] = fma(r[i * S + s], oi, rz[s]);
+            if (exact) prod[static_cast<size_t>(s) * n0 + i] = __dmul_rn(r[i * S + s], oi);
+          }
+        }
       }
     }
     __syncthreads();
+    if (last == 0 && H.dense_n > 0) {  // single dense level: r.z here
+      for (int i = t; i < n0; i += AMG_T)
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          rz[s] = fma(r0[i * S + s], z[i * S + s], rz[s]);
+          if (exact) prod[static_cast<size_t>(s) * n0 + i] = __dmul_rn(r0[i * S + s], z[i * S + s]);
+        }
+      __syncthreads();
+    }
   }
   // ---- up: prolongation, post-smooth ---------------------------------------------
-  double rz = 0.0;
   for (int l = last - 1; l >= 0; --l) {
     const AmgLevelD& L = H.lv[l];
     const double* r = vr(l);
     double* x = vx(l);
-    const double* oc = l + 1 == last && H.dense_n == 0 && last == 0 ? z : vo(l + 1);
+    const double* oc = vo(l + 1);
     for (int i = t; i < L.n; i += AMG_T) {  // x += P coarse (x_i + P_ik c_k, ascending k)
+      double acc[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) acc[s] = x[i * S + s];
       int w;
       int e = ell_row(L.P, i, w);
-      double s = x[i];
       for (int k = 0; k < w; ++k, e += 32) {
         const int c = __ldg(L.P.col + e);
         if (c < 0) break;
-        s = __dadd_rn(s, __dmul_rn(__ldg(L.P.val + e), oc[c]));
+        const double v = __ldg(L.P.val + e);
+#pragma unroll
+        for (int s = 0; s < S; ++s) acc[s] = __dadd_rn(acc[s], __dmul_rn(v, oc[c * S + s]));
       }
-      x[i] = s;
+#pragma unroll
+      for (int s = 0; s < S; ++s) x[i * S + s] = acc[s];
     }
     __syncthreads();
     double* o = l == 0 ? z : vo(l);
     for (int i = t; i < L.n; i += AMG_T) {  // x += omega D^-1 (r - A x), A x into a fresh vector
-      const double ti = ell_dot(L.A, i, x);
-      const double oi = __dadd_rn(x[i], __dmul_rn(omega, __dmul_rn(__ldg(L.inv_diag + i), __dsub_rn(r[i], ti))));
-      o[i] = oi;
-      if (l == 0) {
-        rz = fma(r[i], oi, rz);
-        if (exact) prod[i] = __dmul_rn(r[i], oi);
+      double acc[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) acc[s] = 0.0;
+      int w;
+      int e = ell_row(L.A, i, w);
+      for (int k = 0; k < w; ++k, e += 32) {
+        const int c = __ldg(L.A.col + e);
+        if (c < 0) break;
+        const double a = __ldg(L.A.val + e);
+#pragma unroll
+        for (int s = 0; s < S; ++s) acc[s] = __dadd_rn(acc[s], __dmul_rn(a, x[c * S + s]));
+      }
+      const double di = __ldg(L.inv_diag + i);
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const double ri = r[i * S + s];
+        const double oi = __dadd_rn(x[i * S + s], __dmul_rn(omega, __dmul_rn(di, __dsub_rn(ri, acc[s]))));
+        o[i * S + s] = oi;
+        if (l == 0) {
+          rz[s] = fma(ri, oi, rz[s]);
+          if (exact) prod[static_cast<size_t>(s) * n0 + i] = __dmul_rn(ri, oi);
+        }
       }
     }
     __syncthreads();
   }
-  if (last == 0) {  // single-level hierarchy: the smoother (or the dense solve) wrote z
-    for (int i = t; i < H.lv[0].n; i += AMG_T) {
-      rz = fma(r0[i], z[i], rz);
-      if (exact) prod[i] = __dmul_rn(r0[i], z[i]);
-    }
-    __syncthreads();
-  }
-  return rz;
 }
 
 struct PcgAmgParams {
@@ -192,13 +279,15 @@ struct PcgAmgParams {
   const double* kappa;      // samples x ldk nodal kappa (natural mesh order)
   int64_t ldk;
   const uint8_t* kflag;
-  const int32_t* perm;
+  const int32_t* perm;      // label-major order (groups index into it)
   const int32_t* labels;
+  const int2* groups;       // (first entry in perm, count <= S), one label each
+  const int* ngroups;
   const AmgHierD* hier;     // P hierarchies
   double omega;
-  double* work;             // per CTA: AMG_WORK n + cv_len doubles
-  int64_t cta_stride;       // doubles per CTA
-  int cv_off;               // offset of the coarse-level scratch inside a CTA's block
+  double* work;             // per CTA: cta_stride doubles
+  int64_t cta_stride;
+  int64_t cv_off;           // offset of the coarse-level scratch inside a CTA's block
   int64_t B, out_base, solve_limit;
   double eps;
   int max_iter;
@@ -211,158 +300,298 @@ struct PcgAmgParams {
   int exact;
 };
 
-constexpr int AMG_WORK = 13;  // Ad, Aw, As, b, x[2], r, p[2], z, x0, res0, prod
+constexpr int AMG_WORK = 13;  // per slot: Ad, Aw, As, b, x[2], r, p[2], z, x0, res0, prod
 
-template <int NW>
-__device__ __forceinline__ double amg_reduce(bool exact, double part, const double* prod, int n, double* slot,
-                                             int warp, int lane) {
-  return exact ? serial_sum2d(prod, n, slot) : block_sum2d<NW>(part, slot, warp, lane);
+// block sums of S partials (one reduction round for all slots)
+template <int S>
+__device__ __forceinline__ void amg_block_sums(double (&v)[S], double (*red)[AMG_T / 32], int warp, int lane) {
+#pragma unroll
+  for (int s = 0; s < S; ++s) v[s] = warp_allsum(v[s]);
+  if (lane == 0)
+#pragma unroll
+    for (int s = 0; s < S; ++s) red[s][warp] = v[s];
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    double a[AMG_T / 32];
+#pragma unroll
+    for (int i = 0; i < AMG_T / 32; ++i) a[i] = red[s][i];
+#pragma unroll
+    for (int w = 1; w < AMG_T / 32; w <<= 1)
+#pragma unroll
+      for (int i = 0; i + w < AMG_T / 32; i += 2 * w) a[i] += a[i + w];
+    v[s] = a[0];
+  }
+  __syncthreads();
 }
 
+// exact mode: slot s's products summed serially (s = 0; s += t_i, i = 0..n-1) by thread s
+template <int S>
+__device__ __forceinline__ void amg_serial_sums(double (&v)[S], const double* prod, int n, double* sval) {
+  __syncthreads();
+  if (threadIdx.x < S) {
+    const double* q = prod + static_cast<size_t>(threadIdx.x) * n;
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) acc = __dadd_rn(acc, q[i]);
+    sval[threadIdx.x] = acc;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < S; ++s) v[s] = sval[s];
+  __syncthreads();
+}
+
+// One CTA per group of up to S samples of one label (the centroid's hierarchy is
+// streamed once for all of them); slots that terminate keep iterating with
+// alpha = beta = 0 (their vectors stay put) until the whole group is done.
+template <int S>
 __global__ void __launch_bounds__(AMG_T, 2) pcgamg2d_kernel(const PcgAmgParams prm) {
   constexpr int NW = AMG_T / 32;
-  __shared__ double red[4][NW];
-  __shared__ double sdense[AMG_MAXDENSE];
-  __shared__ int64_t s_item;
+  extern __shared__ double sdense[];  // dense_n * S
+  __shared__ double red[S][NW];
+  __shared__ double sval[S];
+  __shared__ int s_grp;
   const Grid2D g = prm.g;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int n = g.n, m = g.m;
   double* base = prm.work + static_cast<size_t>(blockIdx.x) * prm.cta_stride;
+  const size_t nS = static_cast<size_t>(n) * S;
   double* Ad = base;
-  double* Aw = base + n;       // W coupling of node i; the E coupling of i is Aw[i + 1]
-  double* As = base + 2 * n;   // S coupling of node i; the N coupling of i is As[i + m]
-  double* Bv = base + 3 * n;
-  double* Xb[2] = {base + 4 * n, base + 5 * n};
-  double* Rv = base + 6 * n;
-  double* Pb[2] = {base + 7 * n, base + 8 * n};
-  double* Z = base + 9 * n;
-  double* X0 = base + 10 * n;
-  double* Res0 = base + 11 * n;
-  double* Prod = base + 12 * n;
+  double* Aw = base + nS;       // W coupling of node i; the E coupling of i is Aw[i + 1]
+  double* As = base + 2 * nS;   // S coupling of node i; the N coupling of i is As[i + m]
+  double* Bv = base + 3 * nS;
+  double* Xb[2] = {base + 4 * nS, base + 5 * nS};
+  double* Rv = base + 6 * nS;
+  double* Pb[2] = {base + 7 * nS, base + 8 * nS};
+  double* Z = base + 9 * nS;
+  double* X0 = base + 10 * nS;
+  double* Res0 = base + 11 * nS;
+  double* Prod = base + 12 * nS;  // exact mode: slot s's products at Prod[s * n + i]
   double* cv = base + prm.cv_off;
   const bool exact = prm.exact != 0;
-  auto reduce = [&](double part, double* slot) { return amg_reduce<NW>(exact, part, Prod, n, slot, warp, lane); };
+  auto reduce = [&](double (&v)[S]) {
+    if (exact) amg_serial_sums<S>(v, Prod, n, sval);
+    else amg_block_sums<S>(v, red, warp, lane);
+  };
 
   for (;;) {
-    if (t == 0) s_item = atomicAdd(prm.counter, 1);
+    if (t == 0) s_grp = atomicAdd(prm.counter, 1);
     __syncthreads();
-    const int64_t item = s_item;
+    const int grp = s_grp;
     __syncthreads();
-    if (item >= prm.B) break;
-    const int s = prm.perm[item];
-    const int64_t gs = prm.out_base + s;
-    const int label = prm.labels[s];
-    if (label < 0 || prm.kflag[s] || gs >= prm.solve_limit) {
-      if (t == 0) {
-        prm.iters[gs] = 0;
-        prm.rel[gs] = 0.0;
-        prm.status[gs] = gs >= prm.solve_limit ? VQPC_S_NOT_SOLVED
-                         : label < 0           ? VQPC_S_INVALID_LATENT
-                                               : (prm.kflag[s] & 1) ? VQPC_S_COEFF_OVERFLOW : VQPC_S_INVALID_COEFF;
+    if (grp >= *prm.ngroups) break;
+    const int2 gr = prm.groups[grp];
+    int sid[S], mit[S], J[S];
+    int64_t gsv[S];
+    bool act[S];
+    double rel_rec[S];
+    uint8_t st[S];
+    int label = 0;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      act[s] = false;
+      J[s] = 0;
+      rel_rec[s] = 0.0;
+      st[s] = VQPC_S_MAX_ITER;
+      sid[s] = -1;
+      gsv[s] = 0;
+      mit[s] = 0;
+      if (s < gr.y) {
+        const int sm = prm.perm[gr.x + s];
+        sid[s] = sm;
+        gsv[s] = prm.out_base + sm;
+        const int lb = prm.labels[sm];
+        if (lb < 0 || prm.kflag[sm] || gsv[s] >= prm.solve_limit) {
+          st[s] = gsv[s] >= prm.solve_limit ? VQPC_S_NOT_SOLVED
+                  : lb < 0                  ? VQPC_S_INVALID_LATENT
+                                            : (prm.kflag[sm] & 1) ? VQPC_S_COEFF_OVERFLOW : VQPC_S_INVALID_COEFF;
+        } else {
+          act[s] = true;
+          label = lb;  // a group shares one label (bucketed)
+        }
+        mit[s] = prm.max_iter_arr ? prm.max_iter_arr[gsv[s]] : (prm.max_iter < 0 ? 10 * n : prm.max_iter);
       }
-      continue;
     }
-    const double* kap = prm.kappa + static_cast<size_t>(s) * prm.ldk;
     const AmgHierD& H = prm.hier[label];
     int xc = 0, pc = 0;
 
-    // ---- setup: the sample's rows (fem.cpp:213-256), x = 0, r = b --------------------
-    double bb = 0.0;
+    // ---- setup: every slot's rows (fem.cpp:213-256), x = 0, r = b; idle slots r = 0 ----
+    double part[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) part[s] = 0.0;
     for (int i = t; i < n; i += AMG_T) {
-      const RowCoef rc = assemble_row(kap, g, i % m, i / m);
-      Ad[i] = rc.d;
-      Aw[i] = rc.w;
-      As[i] = rc.s;
-      Bv[i] = rc.b;
-      Xb[0][i] = 0.0;
-      Rv[i] = rc.b;
-      bb = fma(rc.b, rc.b, bb);
-      if (exact) Prod[i] = __dmul_rn(rc.b, rc.b);
-    }
-    __syncthreads();
-    const int max_iter = prm.max_iter_arr ? prm.max_iter_arr[gs] : (prm.max_iter < 0 ? 10 * n : prm.max_iter);
-    const double norm_b = sqrt(reduce(bb, red[3]));
-    double rz = reduce(amg_vcycle(H, prm.omega, Rv, X0, Res0, Z, cv, sdense, exact, Prod), red[2]);
-    int J = 0;
-    double rel_rec = 0.0;
-    uint8_t st = VQPC_S_MAX_ITER;
-    if (norm_b == 0.0) st = VQPC_S_CONVERGED;
-    else if (!(rz > 0.0)) st = VQPC_S_BREAKDOWN;
-    else {
-      double beta = 0.0;
-      for (int j = 1; j <= max_iter; ++j) {
-        // ---- p_new = z + beta p (solver.cpp:241) and A p, p.Ap; neighbours' p_new recomputed
-        const double* Po = Pb[pc];
-        double* Pn = Pb[pc ^ 1];
-        const bool first = j == 1;
-        auto pnew = [&](int q) { return first ? Z[q] : __dadd_rn(Z[q], __dmul_rn(beta, Po[q])); };
-        double pap = 0.0;
-        for (int i = t; i < n; i += AMG_T) {
-          const int ix = i % m, iy = i / m;
-          const double pi = pnew(i);
-          Pn[i] = pi;
-          const double ps = iy > 0 ? pnew(i - m) : 0.0, pw = ix > 0 ? pnew(i - 1) : 0.0;
-          const double pe = ix < m - 1 ? pnew(i + 1) : 0.0, pn = iy < m - 1 ? pnew(i + m) : 0.0;
-          const double ae = ix < m - 1 ? Aw[i + 1] : 0.0, an = iy < m - 1 ? As[i + m] : 0.0;
-          const double ap = row_apply(As[i], Aw[i], Ad[i], ae, an, ps, pw, pi, pe, pn);
-          pap = fma(pi, ap, pap);
-          if (exact) Prod[i] = __dmul_rn(pi, ap);
+      const int ix = i % m, iy = i / m;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        RowCoef rc;
+        if (act[s]) {
+          rc = assemble_row(prm.kappa + static_cast<size_t>(sid[s]) * prm.ldk, g, ix, iy);
+        } else {
+          rc.d = 1.0;
+          rc.w = rc.s = rc.e = rc.nn = rc.b = 0.0;
         }
-        pc ^= 1;
-        const double pAp = reduce(pap, red[0]);
-        if (!(pAp > 0.0)) {
-          st = VQPC_S_BREAKDOWN;
-          break;
-        }
-        const double alpha = rz / pAp;
-        // ---- x += alpha p; r -= alpha A p; r_true = b - A x (solver.cpp:215-222) ----------
-        const double* Pv = Pb[pc];
-        const double* Xo = Xb[xc];
-        double* Xn = Xb[xc ^ 1];
-        auto xnew = [&](int q) { return __dadd_rn(Xo[q], __dmul_rn(alpha, Pv[q])); };
-        double rr = 0.0;
-        for (int i = t; i < n; i += AMG_T) {
-          const int ix = i % m, iy = i / m;
-          const bool hs = iy > 0, hw = ix > 0, he = ix < m - 1, hn = iy < m - 1;
-          const double as = As[i], aw = Aw[i], ad = Ad[i];
-          const double ae = he ? Aw[i + 1] : 0.0, an = hn ? As[i + m] : 0.0;
-          const double ap = row_apply(as, aw, ad, ae, an, hs ? Pv[i - m] : 0.0, hw ? Pv[i - 1] : 0.0, Pv[i],
-                                      he ? Pv[i + 1] : 0.0, hn ? Pv[i + m] : 0.0);
-          const double xi = xnew(i);
-          Xn[i] = xi;
-          Rv[i] = __dsub_rn(Rv[i], __dmul_rn(alpha, ap));
-          const double ax = row_apply(as, aw, ad, ae, an, hs ? xnew(i - m) : 0.0, hw ? xnew(i - 1) : 0.0, xi,
-                                      he ? xnew(i + 1) : 0.0, hn ? xnew(i + m) : 0.0);
-          const double rt = __dsub_rn(Bv[i], ax);
-          rr = fma(rt, rt, rr);
-          if (exact) Prod[i] = __dmul_rn(rt, rt);
-        }
-        xc ^= 1;
-        const double rel = sqrt(reduce(rr, red[1])) / norm_b;
-        J = j;
-        rel_rec = rel;
-        if (rel < prm.eps) {
-          st = VQPC_S_CONVERGED;
-          break;
-        }
-        // ---- z = M^{-1} r (one V-cycle); r.z ------------------------------------------
-        const double rz_next = reduce(amg_vcycle(H, prm.omega, Rv, X0, Res0, Z, cv, sdense, exact, Prod), red[2]);
-        if (!(rz_next > 0.0)) {
-          st = VQPC_S_BREAKDOWN;
-          break;
-        }
-        beta = rz_next / rz;
-        rz = rz_next;
+        const size_t q = static_cast<size_t>(i) * S + s;
+        Ad[q] = rc.d;
+        Aw[q] = rc.w;
+        As[q] = rc.s;
+        Bv[q] = rc.b;
+        Xb[0][q] = 0.0;
+        Rv[q] = rc.b;
+        part[s] = fma(rc.b, rc.b, part[s]);
+        if (exact) Prod[static_cast<size_t>(s) * n + i] = __dmul_rn(rc.b, rc.b);
       }
     }
-    if (t == 0) {
-      prm.iters[gs] = J;
-      prm.rel[gs] = rel_rec;
-      prm.status[gs] = st;
+    __syncthreads();
+    reduce(part);
+    double norm_b[S], rz[S], beta[S], alpha[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) norm_b[s] = sqrt(part[s]);
+    amg_vcycle<S>(H, prm.omega, Rv, X0, Res0, Z, cv, sdense, exact, Prod, rz);
+    reduce(rz);
+    bool any = false;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      beta[s] = alpha[s] = 0.0;
+      if (!act[s]) continue;
+      if (norm_b[s] == 0.0) {
+        st[s] = VQPC_S_CONVERGED;
+        act[s] = false;
+      } else if (!(rz[s] > 0.0)) {
+        st[s] = VQPC_S_BREAKDOWN;
+        act[s] = false;
+      } else if (mit[s] < 1) {
+        act[s] = false;
+      }
+      any |= act[s];
     }
-    if (prm.x_out) {
-      double* xo = prm.x_out + static_cast<size_t>(gs) * n;
-      for (int i = t; i < n; i += AMG_T) xo[i] = Xb[xc][i];
+    for (int j = 1; any; ++j) {
+      // ---- p_new = z + beta p (solver.cpp:241) and A p, p.Ap; neighbours' p_new recomputed
+      const double* Po = Pb[pc];
+      double* Pn = Pb[pc ^ 1];
+      const bool first = j == 1;
+#pragma unroll
+      for (int s = 0; s < S; ++s) part[s] = 0.0;
+      for (int i = t; i < n; i += AMG_T) {
+        const int ix = i % m, iy = i / m;
+        const bool hs = iy > 0, hw = ix > 0, he = ix < m - 1, hn = iy < m - 1;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          auto pnew = [&](int q) {
+            const size_t u = static_cast<size_t>(q) * S + s;
+            return first ? Z[u] : __dadd_rn(Z[u], __dmul_rn(beta[s], Po[u]));
+          };
+          const size_t u = static_cast<size_t>(i) * S + s;
+          const double pi = pnew(i);
+          Pn[u] = pi;
+          const double ae = he ? Aw[u + S] : 0.0, an = hn ? As[u + static_cast<size_t>(m) * S] : 0.0;
+          const double ap = row_apply(As[u], Aw[u], Ad[u], ae, an, hs ? pnew(i - m) : 0.0, hw ? pnew(i - 1) : 0.0, pi,
+                                      he ? pnew(i + 1) : 0.0, hn ? pnew(i + m) : 0.0);
+          part[s] = fma(pi, ap, part[s]);
+          if (exact) Prod[static_cast<size_t>(s) * n + i] = __dmul_rn(pi, ap);
+        }
+      }
+      pc ^= 1;
+      reduce(part);
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        alpha[s] = 0.0;
+        if (!act[s]) continue;
+        if (!(part[s] > 0.0)) {
+          st[s] = VQPC_S_BREAKDOWN;
+          act[s] = false;
+          continue;
+        }
+        alpha[s] = rz[s] / part[s];
+      }
+      // ---- x += alpha p; r -= alpha A p; r_true = b - A x (solver.cpp:215-222) ----------
+      const double* Pv = Pb[pc];
+      const double* Xo = Xb[xc];
+      double* Xn = Xb[xc ^ 1];
+#pragma unroll
+      for (int s = 0; s < S; ++s) part[s] = 0.0;
+      for (int i = t; i < n; i += AMG_T) {
+        const int ix = i % m, iy = i / m;
+        const bool hs = iy > 0, hw = ix > 0, he = ix < m - 1, hn = iy < m - 1;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const size_t u = static_cast<size_t>(i) * S + s, dm = static_cast<size_t>(m) * S;
+          auto xnew = [&](size_t q) { return __dadd_rn(Xo[q], __dmul_rn(alpha[s], Pv[q])); };
+          const double as = As[u], aw = Aw[u], ad = Ad[u];
+          const double ae = he ? Aw[u + S] : 0.0, an = hn ? As[u + dm] : 0.0;
+          const double ap = row_apply(as, aw, ad, ae, an, hs ? Pv[u - dm] : 0.0, hw ? Pv[u - S] : 0.0, Pv[u],
+                                      he ? Pv[u + S] : 0.0, hn ? Pv[u + dm] : 0.0);
+          const double xi = xnew(u);
+          Xn[u] = xi;
+          Rv[u] = __dsub_rn(Rv[u], __dmul_rn(alpha[s], ap));
+          const double ax = row_apply(as, aw, ad, ae, an, hs ? xnew(u - dm) : 0.0, hw ? xnew(u - S) : 0.0, xi,
+                                      he ? xnew(u + S) : 0.0, hn ? xnew(u + dm) : 0.0);
+          const double rt = __dsub_rn(Bv[u], ax);
+          part[s] = fma(rt, rt, part[s]);
+          if (exact) Prod[static_cast<size_t>(s) * n + i] = __dmul_rn(rt, rt);
+        }
+      }
+      xc ^= 1;
+      reduce(part);
+      bool need = false;
+      bool done_now[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        done_now[s] = false;
+        if (!act[s]) continue;
+        const double rel = sqrt(part[s]) / norm_b[s];
+        J[s] = j;
+        rel_rec[s] = rel;
+        if (rel < prm.eps) {
+          st[s] = VQPC_S_CONVERGED;
+          act[s] = false;
+          done_now[s] = true;
+        } else if (j >= mit[s]) {  // loop exhausted: MAX_ITER (x is this iterate)
+          act[s] = false;
+          done_now[s] = true;
+        } else {
+          need = true;
+        }
+      }
+      if (prm.x_out) {  // a slot's x at its exit iteration (later iterations leave it with alpha = 0 anyway)
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+          if (done_now[s]) {
+            double* xo = prm.x_out + static_cast<size_t>(gsv[s]) * n;
+            for (int i = t; i < n; i += AMG_T) xo[i] = Xn[static_cast<size_t>(i) * S + s];
+          }
+      }
+      if (!need) break;
+      // ---- z = M^{-1} r (one V-cycle for every slot); r.z -----------------------------
+      amg_vcycle<S>(H, prm.omega, Rv, X0, Res0, Z, cv, sdense, exact, Prod, part);
+      reduce(part);
+      any = false;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        beta[s] = 0.0;
+        if (!act[s]) continue;
+        if (!(part[s] > 0.0)) {
+          st[s] = VQPC_S_BREAKDOWN;
+          act[s] = false;
+          continue;
+        }
+        beta[s] = part[s] / rz[s];
+        rz[s] = part[s];
+        any = true;
+      }
+    }
+    // slots whose solve ended in a breakdown (or never started) report x as it stands
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      if (s >= gr.y) continue;
+      if (t == 0) {
+        prm.iters[gsv[s]] = J[s];
+        prm.rel[gsv[s]] = rel_rec[s];
+        prm.status[gsv[s]] = st[s];
+      }
+      if (prm.x_out && (st[s] == VQPC_S_BREAKDOWN)) {
+        double* xo = prm.x_out + static_cast<size_t>(gsv[s]) * n;
+        for (int i = t; i < n; i += AMG_T) xo[i] = Xb[xc][static_cast<size_t>(i) * S + s];
+      }
     }
     __syncthreads();
   }
@@ -371,8 +600,9 @@ __global__ void __launch_bounds__(AMG_T, 2) pcgamg2d_kernel(const PcgAmgParams p
 // M^{-1} r for one vector (Preconditioner::apply; parity tests), one CTA
 __global__ void __launch_bounds__(AMG_T) amg_apply_kernel(const AmgHierD* hier, int p, double omega, const double* r,
                                                           double* z, double* x0, double* res0, double* cv) {
-  __shared__ double sdense[AMG_MAXDENSE];
-  amg_vcycle(hier[p], omega, r, x0, res0, z, cv, sdense, false, nullptr);
+  extern __shared__ double sdense[];
+  double rz[1];
+  amg_vcycle<1>(hier[p], omega, r, x0, res0, z, cv, sdense, false, nullptr, rz);
 }
 
 // CSR values of the 2-D centroid matrices in the reference's stored pattern

@@ -127,7 +127,8 @@ struct vqpc_ctx {
   DBuf<int> amg_i;
   DBuf<double> amg_d, amg_work;
   DBuf<AmgHierD> amg_hd;
-  int amg_cv = 0;           // doubles of coarse-level scratch per CTA (max over centroids)
+  int amg_cv = 0;           // doubles of coarse-level scratch per CTA and slot (max over centroids)
+  int amg_dense_max = 0;    // largest coarsest dense size over the centroids
   int64_t amg_entries = 0;  // stored hierarchy entries per centroid (mean), roofline accounting
   cudaStream_t aux = nullptr;              // chunks beyond the solve subset (overlap with the PCG)
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
@@ -499,15 +500,43 @@ void run_pcgchol2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_
   launch_check(c);
 }
 
+// SA-AMG kind: label-major order (stable over the cost-ordered queue), groups of up
+// to S same-label samples (the centroid's hierarchy is streamed once per group),
+// one persistent CTA per group.
+template <int S>
+void launch_pcgamg2d(vqpc_ctx* c, PcgAmgParams& prm, int64_t ngroups_max) {
+  const size_t smem = sizeof(double) * static_cast<size_t>(std::max(c->amg_dense_max, 1)) * S;
+  CK(cudaFuncSetAttribute(pcgamg2d_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcgamg2d_kernel<S>, AMG_T, smem));
+  if (per_sm < 1) throw ApiError{VQPC_CUDA_ERROR, "pcgamg2d kernel does not fit on an SM"};
+  const int64_t blocks = cap_groups(std::min<int64_t>(ngroups_max, static_cast<int64_t>(per_sm) * c->sm_count));
+  prm.cv_off = static_cast<int64_t>(AMG_WORK) * c->n * S;
+  prm.cta_stride = prm.cv_off + static_cast<int64_t>(c->amg_cv) * S + 2;
+  c->amg_work.ensure(static_cast<size_t>(blocks) * prm.cta_stride);
+  prm.work = c->amg_work.p;
+  Timed tm(c, VQPC_K_PCG);
+  pcgamg2d_kernel<S><<<static_cast<unsigned>(blocks), AMG_T, smem, c->stream>>>(prm);
+  launch_check(c);
+}
+
 void run_pcgamg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d_kflag, const int32_t* d_perm,
                   const int32_t* d_labels, int64_t B, int64_t out_base, double eps, int max_iter, const int32_t* d_mia,
                   int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x, int64_t solve_limit) {
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcgamg2d_kernel, AMG_T, 0));
-  if (per_sm < 1) throw ApiError{VQPC_CUDA_ERROR, "pcgamg2d kernel does not fit on an SM"};
-  const int64_t blocks = cap_groups(std::min<int64_t>(B, static_cast<int64_t>(per_sm) * c->sm_count));
-  const int64_t stride = static_cast<int64_t>(AMG_WORK) * c->n + c->amg_cv + 2;
-  c->amg_work.ensure(static_cast<size_t>(blocks) * stride);
+  const int P = c->pb.P;
+  int S = 4;  // samples per CTA (VQPC_AMG_S overrides: 1, 2, 4, 8)
+  if (const char* e = getenv("VQPC_AMG_S")) S = atoi(e);
+  S = S >= 8 ? 8 : S >= 4 ? 4 : S >= 2 ? 2 : 1;
+  c->ch_perm.ensure(B);
+  c->ch_off.ensure(P + 2);
+  c->ch_groups.ensure(B + P + 1);
+  c->ch_ngroups.ensure(1);
+  {
+    Timed tm(c, VQPC_K_BUCKET);
+    counting_sort(c, d_labels, d_perm, B, P, c->ch_perm.p, c->ch_off.p);
+    chol_groups_kernel<<<1, CG_T, 0, c->stream>>>(c->ch_off.p, P, S, c->ch_groups.p, c->ch_ngroups.p);
+    launch_check(c);
+  }
   c->counter.ensure(1);
   CK(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->stream));
   PcgAmgParams prm{};
@@ -515,13 +544,12 @@ void run_pcgamg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t
   prm.kappa = d_kappa;
   prm.ldk = ldk;
   prm.kflag = d_kflag;
-  prm.perm = d_perm;
+  prm.perm = c->ch_perm.p;
   prm.labels = d_labels;
+  prm.groups = c->ch_groups.p;
+  prm.ngroups = c->ch_ngroups.p;
   prm.hier = c->amg_hd.p;
   prm.omega = 2.0 / 3.0;  // AmgOptions::jacobi_weight (solver.hpp:37)
-  prm.work = c->amg_work.p;
-  prm.cta_stride = stride;
-  prm.cv_off = AMG_WORK * c->n;
   prm.B = B;
   prm.out_base = out_base;
   prm.solve_limit = solve_limit;
@@ -534,9 +562,13 @@ void run_pcgamg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t
   prm.status = d_status;
   prm.x_out = d_x;
   prm.exact = c->exact;
-  Timed tm(c, VQPC_K_PCG);
-  pcgamg2d_kernel<<<static_cast<unsigned>(blocks), AMG_T, 0, c->stream>>>(prm);
-  launch_check(c);
+  const int64_t ng = ceil_div(B, S) + P + 1;
+  switch (S) {
+    case 8: launch_pcgamg2d<8>(c, prm, ng); break;
+    case 4: launch_pcgamg2d<4>(c, prm, ng); break;
+    case 2: launch_pcgamg2d<2>(c, prm, ng); break;
+    default: launch_pcgamg2d<1>(c, prm, ng); break;
+  }
 }
 
 void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d_kflag, const int32_t* d_perm,
@@ -1076,6 +1108,8 @@ void setup_amg(vqpc_ctx* c, const double* d_kc, int64_t ldk, int P) {
   CK(cudaStreamSynchronize(c->stream));
   c->amg_cv = (cv_max + 1) & ~1;
   c->amg_entries = entries / P;
+  c->amg_dense_max = 0;
+  for (int p = 0; p < P; ++p) c->amg_dense_max = std::max(c->amg_dense_max, hh[p].dense_n);
 }
 
 // Factor P coefficient fields (d_kc: P rows of ldk nodal/elemental values) into the
@@ -1474,7 +1508,8 @@ int vqpc_precond_apply(vqpc_ctx* c, int p, const double* r, double* z) {
     if (c->amg) {
       c->dvec.ensure(5 * static_cast<size_t>(c->n) + c->amg_cv);
       h2d(c, c->dvec.p, r, c->n);
-      amg_apply_kernel<<<1, AMG_T, 0, c->stream>>>(c->amg_hd.p, p, 2.0 / 3.0, c->dvec.p, c->dvec.p + c->n,
+      amg_apply_kernel<<<1, AMG_T, sizeof(double) * std::max(c->amg_dense_max, 1), c->stream>>>(
+          c->amg_hd.p, p, 2.0 / 3.0, c->dvec.p, c->dvec.p + c->n,
                                                    c->dvec.p + 2 * c->n, c->dvec.p + 3 * c->n, c->dvec.p + 5 * c->n);
     } else if (c->chol2d)
       cholapply_serial_kernel<<<1, 1, 0, c->stream>>>(c->ch_L.p, c->ch_ldL, c->clay, p, c->dvec.p,
@@ -1798,6 +1833,7 @@ int vqpc_ideal_sweep(vqpc_ctx* c, const double* xi, int64_t B, int ld, const int
       std::swap(c->amg_h, o.amg_h);
       std::swap(c->amg_cv, o.amg_cv);
       std::swap(c->amg_entries, o.amg_entries);
+      std::swap(c->amg_dense_max, o.amg_dense_max);
       std::swap(c->fac_lu, o.fac_lu);
       std::swap(c->have_lu, o.have_lu);
     };
