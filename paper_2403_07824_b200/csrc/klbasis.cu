@@ -75,15 +75,18 @@ bool tridiagonal_ql(std::vector<double>& d, std::vector<double> e, std::vector<d
   Z.assign(static_cast<size_t>(k) * k, 0.0);
   for (int i = 0; i < k; ++i) Z[static_cast<size_t>(i) * k + i] = 1.0;
   e.resize(k, 0.0);
+  double tnorm = 0.0;  // deflation floor: off-diagonals below eps * ||T|| are zero (the noise-level
+  for (int i = 0; i < k; ++i) tnorm = std::max(tnorm, std::abs(d[i]) + std::abs(e[i]));  // tail of T)
+  const double floor_e = 1e-17 * tnorm;
   for (int l = 0; l < k; ++l) {
     int iter = 0, m;
     do {
       for (m = l; m < k - 1; ++m) {
         const double dd = std::abs(d[m]) + std::abs(d[m + 1]);
-        if (std::abs(e[m]) <= 1e-17 * dd) break;
+        if (std::abs(e[m]) <= 1e-17 * dd || std::abs(e[m]) <= floor_e) break;
       }
       if (m != l) {
-        if (++iter > 200) return false;
+        if (++iter > 1000) return false;
         double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
         double r = std::hypot(g, 1.0);
         g = d[m] - d[l] + e[l] / (g + (g >= 0 ? std::abs(r) : -std::abs(r)));

@@ -137,6 +137,9 @@ struct vqpc_ctx {
   int exact = 0;  // reference-order mode: serial dot products (2-D); 1-D: pcg1d_exact_kernel
   DBuf<double2> fac_lu;  // 1-D reference-order mode: P x NP {l_j, u_j}, built on first use
   bool have_lu = false;
+  const double* lu_src = nullptr;  // the coefficients the current factors were built from (factor_coefficients)
+  int64_t lu_ld = 0;
+  int lu_count = 0;
   DBuf<double> work1x;
   // work buffers
   DBuf<double> xi, kappa, best, dvec;
@@ -646,13 +649,13 @@ void run_pcg1d_exact(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint
                      const int32_t* d_labels, int64_t B, int64_t out_base, double eps, int max_iter,
                      const int32_t* d_mia, int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x,
                      int64_t solve_limit) {
-  const int P = c->pb.P, n = c->n;
+  const int P = c->lu_count, n = c->n;
   if (!c->have_lu) {
     c->fac_lu.ensure(static_cast<size_t>(P) * c->NP);
     CK(cudaMemsetAsync(c->err.p, 0, sizeof(int), c->stream));
     Timed tm(c, VQPC_K_OTHER);
     factor1d_kernel<<<static_cast<unsigned>(ceil_div(P, 64)), 64, 0, c->stream>>>(
-        c->kappa_c.p, (c->pb.n_nodes + 1) & ~1, P, n, h_of(c->pb), c->fac.p, c->NP, c->err.p, c->fac_lu.p);
+        c->lu_src, c->lu_ld, P, n, h_of(c->pb), c->fac.p, c->NP, c->err.p, c->fac_lu.p);
     launch_check(c);
     c->have_lu = true;
   }
@@ -1118,6 +1121,10 @@ void setup_amg(vqpc_ctx* c, const double* d_kc, int64_t ldk, int P) {
 // factor per realisation (driver.cpp:317-320). Throws not-spd.
 void factor_coefficients(vqpc_ctx* c, const double* d_kc, int64_t ldk, int P) {
   const vqpc_problem& pb = c->pb;
+  c->lu_src = d_kc;  // the 1-D reference-order mode rebuilds its {l_j, u_j} from these on first use
+  c->lu_ld = ldk;
+  c->lu_count = P;
+  c->have_lu = false;
     c->err.ensure(1);
     CK(cudaMemsetAsync(c->err.p, 0, sizeof(int), c->stream));
     if (pb.dim == 2 && c->chol2d) {
@@ -1836,6 +1843,9 @@ int vqpc_ideal_sweep(vqpc_ctx* c, const double* xi, int64_t B, int ld, const int
       std::swap(c->amg_dense_max, o.amg_dense_max);
       std::swap(c->fac_lu, o.fac_lu);
       std::swap(c->have_lu, o.have_lu);
+      std::swap(c->lu_src, o.lu_src);
+      std::swap(c->lu_ld, o.lu_ld);
+      std::swap(c->lu_count, o.lu_count);
     };
     vqpc_ctx saved;
     swap_factors(saved);

@@ -7,7 +7,8 @@ import shutil
 import sys
 import time
 
-from paper_2403_07824_b200 import campaign
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2403_07824_b200 import campaign  # noqa: E402
 
 names = sys.argv[1:] or ["C1", "C2", "C3", "C5"]
 out = os.path.join(campaign.ROOT, "gpurun_out", "artifacts")
