@@ -7,6 +7,26 @@
 
 #define VQPC_FULL_MASK 0xffffffffu
 
+// Device-side bounds and invariant checks of the check build (-DVQPC_CHECKS,
+// tools/checks_build.sh): a violated condition prints its location and traps, so
+// the test that triggered it fails loudly. Compiled out of the product build. (The
+// pool's compute-sanitizer is disabled; this build is the memory-safety evidence.)
+#ifdef VQPC_CHECKS
+#include <cstdio>
+#define VQPC_DCHECK(cond)                                                                     \
+  do {                                                                                        \
+    if (!(cond)) {                                                                            \
+      printf("VQPC_DCHECK failed at %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                    \
+      __trap();                                                                               \
+    }                                                                                         \
+  } while (0)
+#else
+#define VQPC_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
+
 namespace vqpc {
 
 // double shuffles (two 32-bit SHFLs each)

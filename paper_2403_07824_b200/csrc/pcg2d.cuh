@@ -545,6 +545,7 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
           if (l - t > 0) v = __dsub_rn(v, __dmul_rn(op[P2_T], sbuf[prv][t + 1]));
           if (t > 0) v = __dsub_rn(v, __dmul_rn(op[2 * P2_T], sbuf[prv][t]));
           v = div_by_pivot(v, op[3 * P2_T], op[4 * P2_T]);
+          VQPC_DCHECK(ac >= 0 && ac < n);
           Y[ac] = v;
           sbuf[cur][t + 1] = v;
         }
@@ -577,6 +578,7 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
           if (l - t < m - 1) acc = __dadd_rn(acc, __dmul_rn(op[0], sbuf[prv][t + 1]));
           if (t < m - 1) acc = __dadd_rn(acc, __dmul_rn(op[P2_T], sbuf[prv][t + 2]));
           const double z = __dsub_rn(op[3 * P2_T], div_by_pivot(acc, op[2 * P2_T], op[5 * P2_T]));
+          VQPC_DCHECK(ac >= 0 && ac < n);
           Z[ac] = z;
           sbuf[cur][t + 1] = z;
           rz_part = fma(op[4 * P2_T], z, rz_part);

@@ -31,11 +31,15 @@ constexpr int AMG_MAXLEV = 16;      // hierarchy depth handled on the device
 constexpr int AMG_MAXDENSE = 1024;  // coarsest dense solve size (shared-memory vector)
 
 // Sliced ELL: rows in slices of 32; slice s holds width_s = (soff[s+1]-soff[s])/32
-// entries per row, entry k of row i at soff[s] + 32 k + (i & 31); col -1 pads.
+// entries per row, entry k of row i at soff[s] + 32 k + (i & 31) for k < rlen[i]
+// (col -1 pads the rest). The row loops run to rlen[i] with no exit that depends on
+// a loaded column, so the unrolled iterations' loads issue together.
 struct AmgEll {
   const int* soff;
   const int* col;
   const double* val;
+  const int* rlen;          // stored entries of each row (the loops end there: no data-dependent exit)
+  int rows, cols;           // shape (bounds checks of the check build)
 };
 
 struct AmgLevelD {
@@ -51,24 +55,10 @@ struct AmgHierD {
   AmgLevelD lv[AMG_MAXLEV];
 };
 
-__device__ __forceinline__ int ell_row(const AmgEll& M, int i, int& width) {
-  const int s = i >> 5;
-  const int b = __ldg(M.soff + s);
-  width = (__ldg(M.soff + s + 1) - b) >> 5;
-  return b + (i & 31);
-}
-
-// y = 0 + sum_k v_k x[c_k] (ascending columns): Eigen's sparse * dense into a fresh vector
-__device__ __forceinline__ double ell_dot(const AmgEll& M, int i, const double* x) {
-  int w;
-  int e = ell_row(M, i, w);
-  double s = 0.0;
-  for (int k = 0; k < w; ++k, e += 32) {
-    const int c = __ldg(M.col + e);
-    if (c < 0) break;
-    s = __dadd_rn(s, __dmul_rn(__ldg(M.val + e), x[c]));
-  }
-  return s;
+__device__ __forceinline__ int ell_row(const AmgEll& M, int i, int& len) {
+  VQPC_DCHECK(i >= 0 && i < M.rows);
+  len = __ldg(M.rlen + i);
+  return __ldg(M.soff + (i >> 5)) + (i & 31);
 }
 
 // ---- one V-cycle z = M^{-1} r for S right-hand sides on hierarchy H ---------------
@@ -91,7 +81,7 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
   for (int s = 0; s < S; ++s) rz[s] = 0.0;
   // ---- down: pre-smooth from zero, residual, restriction -------------------------
   for (int l = 0; l < last; ++l) {
-    const AmgLevelD& L = H.lv[l];
+    const AmgLevelD L = H.lv[l];
     const double* r = vr(l);
     double* x = vx(l);
     double* res = vo(l);  // the residual; later this level's output
@@ -106,9 +96,10 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
       // res = r; res -= A x (Eigen's rewrite of `r - A x`), x_c recomputed with its owner's operations
       int w;
       int e = ell_row(L.A, i, w);
+      #pragma unroll 4
       for (int k = 0; k < w; ++k, e += 32) {
         const int c = __ldg(L.A.col + e);
-        if (c < 0) break;
+        VQPC_DCHECK(c < L.A.cols);
         const double a = __ldg(L.A.val + e), dc = __ldg(L.inv_diag + c);
 #pragma unroll
         for (int s = 0; s < S; ++s)
@@ -125,9 +116,10 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
       for (int s = 0; s < S; ++s) acc[s] = 0.0;
       int w;
       int e = ell_row(L.Pt, c, w);
+      #pragma unroll 4
       for (int k = 0; k < w; ++k, e += 32) {
         const int q = __ldg(L.Pt.col + e);
-        if (q < 0) break;
+        VQPC_DCHECK(q < L.Pt.cols);
         const double v = __ldg(L.Pt.val + e);
 #pragma unroll
         for (int s = 0; s < S; ++s) acc[s] = __dadd_rn(acc[s], __dmul_rn(v, res[q * S + s]));
@@ -139,11 +131,12 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
   }
   // ---- coarsest ----------------------------------------------------------------
   {
-    const AmgLevelD& L = H.lv[last];
+    const AmgLevelD L = H.lv[last];
     const double* r = vr(last);
     double* o = last == 0 ? z : vo(last);
     if (H.dense_n > 0) {
       const int nc = H.dense_n;
+      VQPC_DCHECK(nc == L.n && nc <= AMG_MAXDENSE);
       if (warp == 0) {  // column-oriented substitutions, S right-hand sides, rows dealt to lanes
         for (int q = lane; q < nc * S; q += 32) sdense[q] = r[q];
         __syncwarp();
@@ -191,9 +184,9 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
         for (int s = 0; s < S; ++s) acc[s] = 0.0;
         int w;
         int e = ell_row(L.A, i, w);
+        #pragma unroll 4
         for (int k = 0; k < w; ++k, e += 32) {
           const int c = __ldg(L.A.col + e);
-          if (c < 0) break;
           const double a = __ldg(L.A.val + e);
 #pragma unroll
           for (int s = 0; s < S; ++s) acc[s] = __dadd_rn(acc[s], __dmul_rn(a, x[c * S + s]));
@@ -223,7 +216,7 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
   }
   // ---- up: prolongation, post-smooth ---------------------------------------------
   for (int l = last - 1; l >= 0; --l) {
-    const AmgLevelD& L = H.lv[l];
+    const AmgLevelD L = H.lv[l];
     const double* r = vr(l);
     double* x = vx(l);
     const double* oc = vo(l + 1);
@@ -233,9 +226,10 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
       for (int s = 0; s < S; ++s) acc[s] = x[i * S + s];
       int w;
       int e = ell_row(L.P, i, w);
+      #pragma unroll 4
       for (int k = 0; k < w; ++k, e += 32) {
         const int c = __ldg(L.P.col + e);
-        if (c < 0) break;
+        VQPC_DCHECK(c < L.P.cols);
         const double v = __ldg(L.P.val + e);
 #pragma unroll
         for (int s = 0; s < S; ++s) acc[s] = __dadd_rn(acc[s], __dmul_rn(v, oc[c * S + s]));
@@ -251,9 +245,10 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
       for (int s = 0; s < S; ++s) acc[s] = 0.0;
       int w;
       int e = ell_row(L.A, i, w);
+      #pragma unroll 4
       for (int k = 0; k < w; ++k, e += 32) {
         const int c = __ldg(L.A.col + e);
-        if (c < 0) break;
+        VQPC_DCHECK(c < L.A.cols);
         const double a = __ldg(L.A.val + e);
 #pragma unroll
         for (int s = 0; s < S; ++s) acc[s] = __dadd_rn(acc[s], __dmul_rn(a, x[c * S + s]));

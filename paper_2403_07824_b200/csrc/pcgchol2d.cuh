@@ -400,6 +400,7 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
       if (lane == 0) pc_mbar_expect(bar, PC_LIB * 8u + cbytes + (zin ? S * 256u : 0u));
       __syncwarp();
       auto sa = [](const void* q) { return static_cast<unsigned>(__cvta_generic_to_shared(q)); };
+      VQPC_DCHECK(cbytes <= 8u * static_cast<unsigned>(prm.cap) && (cbytes & 15u) == 0 && (a0 & 1) == 0);
       if (lane == 0) {
         pc_bulk_g2s(sa(sp + PC_LIB), Lp + a0, cbytes, bar);
       } else if (lane == 1) {
@@ -428,6 +429,7 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
         const double* Li = dsm + stg * stage_len;
         const int* meta = reinterpret_cast<const int*>(Li + PC_STG_META);  // first[32], off[32]
         const double* ch = Li + PC_LIB;  // L(r0 + i, j) = ch[off[i] + j]
+        VQPC_DCHECK(r1 - r0 <= PC_BS && lay.W + 3 * PC_BS <= RING);
         int64_t na0 = 0;
         unsigned nby = 0;
         if (warp == 0 && v + 2 < nvis) {  // next issue's source range, loaded while this visit computes

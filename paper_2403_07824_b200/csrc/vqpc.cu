@@ -527,7 +527,7 @@ void run_pcgamg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t
                   const int32_t* d_labels, int64_t B, int64_t out_base, double eps, int max_iter, const int32_t* d_mia,
                   int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x, int64_t solve_limit) {
   const int P = c->pb.P;
-  int S = 4;  // samples per CTA (VQPC_AMG_S overrides: 1, 2, 4, 8)
+  int S = 2;  // samples per CTA (VQPC_AMG_S overrides: 1, 2, 4, 8)
   if (const char* e = getenv("VQPC_AMG_S")) S = atoi(e);
   S = S >= 8 ? 8 : S >= 4 ? 4 : S >= 2 ? 2 : 1;
   c->ch_perm.ensure(B);
@@ -1028,9 +1028,9 @@ void setup_amg(vqpc_ctx* c, const double* d_kc, int64_t ldk, int P) {
   // pack: ints (slice offsets + columns) and doubles (values, inverse diagonals, dense L)
   std::vector<int> hi;
   std::vector<double> hd;
-  struct EllOff { size_t soff, col, val; };
+  struct EllOff { size_t soff, col, val, rlen; };
   auto pack_ell = [&](const amg::Csr& M) {
-    EllOff o{hi.size(), 0, 0};
+    EllOff o{hi.size(), 0, 0, 0};
     const int ns = (M.rows + 31) / 32;
     std::vector<int> soff(ns + 1, 0);
     for (int s = 0; s < ns; ++s) {
@@ -1039,6 +1039,8 @@ void setup_amg(vqpc_ctx* c, const double* d_kc, int64_t ldk, int P) {
       soff[s + 1] = soff[s] + 32 * w;
     }
     hi.insert(hi.end(), soff.begin(), soff.end());
+    o.rlen = hi.size();
+    for (int i = 0; i < M.rows; ++i) hi.push_back(M.ptr[i + 1] - M.ptr[i]);
     o.col = hi.size();
     o.val = hd.size();
     hi.resize(hi.size() + soff[ns], -1);
@@ -1091,16 +1093,16 @@ void setup_amg(vqpc_ctx* c, const double* d_kc, int64_t ldk, int P) {
   c->amg_d.ensure(hd.size());
   h2d(c, c->amg_i.p, hi.data(), hi.size());
   h2d(c, c->amg_d.p, hd.data(), hd.size());
-  auto ell_ptr = [&](const EllOff& o) {
-    return AmgEll{c->amg_i.p + o.soff, c->amg_i.p + o.col, c->amg_d.p + o.val};
+  auto ell_ptr = [&](const EllOff& o, int rows, int cols) {
+    return AmgEll{c->amg_i.p + o.soff, c->amg_i.p + o.col, c->amg_d.p + o.val, c->amg_i.p + o.rlen, rows, cols};
   };
   for (int p = 0; p < P; ++p) {
     for (int l = 0; l < hh[p].nlev; ++l) {
       AmgLevelD& d = hh[p].lv[l];
-      d.A = ell_ptr(lo[p][l].A);
+      d.A = ell_ptr(lo[p][l].A, d.n, d.n);
       if (d.nc) {
-        d.P = ell_ptr(lo[p][l].P);
-        d.Pt = ell_ptr(lo[p][l].Pt);
+        d.P = ell_ptr(lo[p][l].P, d.n, d.nc);
+        d.Pt = ell_ptr(lo[p][l].Pt, d.nc, d.n);
       }
       d.inv_diag = c->amg_d.p + lo[p][l].inv;
     }

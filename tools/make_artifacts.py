@@ -19,6 +19,12 @@ for name in names:
     arts = campaign.prepare_campaign(cfg)
     print(name, "basis", arts["basis"]["eigenvalues"].size, "P", arts["codebook"]["P"], f"{time.time() - t:.1f}s",
           flush=True)
-for f in os.listdir(campaign.CACHE):
-    shutil.copy(os.path.join(campaign.CACHE, f), out)
+keep = set()
+for name in names:  # only the requested configurations' files (gpurun brings back <= 64 MiB)
+    cfg = campaign.CONFIGS[name]
+    keep.add(f"basis_{campaign._key(cfg, 'basis')}.klb")
+    keep.add(f"codebook_{campaign._key(cfg, 'codebook')}.qnt")
+for f in sorted(keep):
+    if os.path.exists(os.path.join(campaign.CACHE, f)):
+        shutil.copy(os.path.join(campaign.CACHE, f), out)
 print("copied", os.listdir(out))
