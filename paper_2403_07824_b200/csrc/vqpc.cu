@@ -527,7 +527,7 @@ void run_pcgamg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t
                   const int32_t* d_labels, int64_t B, int64_t out_base, double eps, int max_iter, const int32_t* d_mia,
                   int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x, int64_t solve_limit) {
   const int P = c->pb.P;
-  int S = 2;  // samples per CTA (VQPC_AMG_S overrides: 1, 2, 4, 8)
+  int S = 1;  // samples per CTA (VQPC_AMG_S overrides: 1, 2, 4, 8; 1 measured fastest)
   if (const char* e = getenv("VQPC_AMG_S")) S = atoi(e);
   S = S >= 8 ? 8 : S >= 4 ? 4 : S >= 2 ? 2 : 1;
   c->ch_perm.ensure(B);

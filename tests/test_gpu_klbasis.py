@@ -64,8 +64,8 @@ def test_gpu_kl_basis_eigen_residuals(name):
     lam = dev["eigenvalues"]
     worst = 0.0
     for k in range(lam.size):
-        v = sm * dev["eigenvectors"][k]
-        V = v.reshape(side, side)
+        v = sm * dev["eigenvectors"][k]  # W = M^1/2 C M^1/2, C = sigma^2 C1 (x) C1
+        V = (sm * v).reshape(side, side)
         Wv = sm * (cfg["sigma2"] * (C1 @ V @ C1.T)).reshape(-1)
         worst = max(worst, np.linalg.norm(Wv - lam[k] * v) / lam[0])
     print(name, f"device KL basis: {lam.size} modes, max ||W v - lambda v|| / lambda_1 = {worst:.2e}")
