@@ -29,6 +29,13 @@ namespace vqpc {
 constexpr int AMG_T = 256;          // threads per CTA
 constexpr int AMG_MAXLEV = 16;      // hierarchy depth handled on the device
 constexpr int AMG_MAXDENSE = 1024;  // coarsest dense solve size (shared-memory vector)
+#ifndef AMG_ROWU
+#define AMG_ROWU 1                   // rows per thread interleaved in the V-cycle passes (A/B builds)
+#endif
+constexpr int kAmgRowU = AMG_ROWU;
+#ifndef AMG_MINB
+#define AMG_MINB 2                   // resident CTAs per SM the register budget targets (A/B builds)
+#endif
 
 // Sliced ELL: rows in slices of 32; slice s holds width_s = (soff[s+1]-soff[s])/32
 // entries per row, entry k of row i at soff[s] + 32 k + (i & 31) for k < rlen[i]
@@ -82,9 +89,10 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
   // ---- down: pre-smooth from zero, residual, restriction -------------------------
   for (int l = 0; l < last; ++l) {
     const AmgLevelD L = H.lv[l];
-    const double* r = vr(l);
-    double* x = vx(l);
-    double* res = vo(l);  // the residual; later this level's output
+    const double* __restrict__ r = vr(l);
+    double* __restrict__ x = vx(l);
+    double* __restrict__ res = vo(l);  // the residual; later this level's output
+#pragma unroll kAmgRowU
     for (int i = t; i < L.n; i += AMG_T) {
       const double di = __ldg(L.inv_diag + i);
       double acc[S];
@@ -109,7 +117,9 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
       for (int s = 0; s < S; ++s) res[i * S + s] = acc[s];
     }
     __syncthreads();
-    double* rn = vr(l + 1);
+    double* __restrict__ rn = vr(l + 1);
+    const double* __restrict__ rs = res;
+#pragma unroll kAmgRowU
     for (int c = t; c < L.nc; c += AMG_T) {  // P^T residual: 0 + sum, ascending fine rows
       double acc[S];
 #pragma unroll
@@ -122,7 +132,7 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
         VQPC_DCHECK(q < L.Pt.cols);
         const double v = __ldg(L.Pt.val + e);
 #pragma unroll
-        for (int s = 0; s < S; ++s) acc[s] = __dadd_rn(acc[s], __dmul_rn(v, res[q * S + s]));
+        for (int s = 0; s < S; ++s) acc[s] = __dadd_rn(acc[s], __dmul_rn(v, rs[q * S + s]));
       }
 #pragma unroll
       for (int s = 0; s < S; ++s) rn[c * S + s] = acc[s];
@@ -217,9 +227,10 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
   // ---- up: prolongation, post-smooth ---------------------------------------------
   for (int l = last - 1; l >= 0; --l) {
     const AmgLevelD L = H.lv[l];
-    const double* r = vr(l);
-    double* x = vx(l);
-    const double* oc = vo(l + 1);
+    const double* __restrict__ r = vr(l);
+    double* __restrict__ x = vx(l);
+    const double* __restrict__ oc = vo(l + 1);
+#pragma unroll kAmgRowU
     for (int i = t; i < L.n; i += AMG_T) {  // x += P coarse (x_i + P_ik c_k, ascending k)
       double acc[S];
 #pragma unroll
@@ -238,7 +249,9 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
       for (int s = 0; s < S; ++s) x[i * S + s] = acc[s];
     }
     __syncthreads();
-    double* o = l == 0 ? z : vo(l);
+    double* __restrict__ o = l == 0 ? z : vo(l);
+    const double* __restrict__ xs = x;
+#pragma unroll kAmgRowU
     for (int i = t; i < L.n; i += AMG_T) {  // x += omega D^-1 (r - A x), A x into a fresh vector
       double acc[S];
 #pragma unroll
@@ -251,13 +264,13 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
         VQPC_DCHECK(c < L.A.cols);
         const double a = __ldg(L.A.val + e);
 #pragma unroll
-        for (int s = 0; s < S; ++s) acc[s] = __dadd_rn(acc[s], __dmul_rn(a, x[c * S + s]));
+        for (int s = 0; s < S; ++s) acc[s] = __dadd_rn(acc[s], __dmul_rn(a, xs[c * S + s]));
       }
       const double di = __ldg(L.inv_diag + i);
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         const double ri = r[i * S + s];
-        const double oi = __dadd_rn(x[i * S + s], __dmul_rn(omega, __dmul_rn(di, __dsub_rn(ri, acc[s]))));
+        const double oi = __dadd_rn(xs[i * S + s], __dmul_rn(omega, __dmul_rn(di, __dsub_rn(ri, acc[s]))));
         o[i * S + s] = oi;
         if (l == 0) {
           rz[s] = fma(ri, oi, rz[s]);
@@ -340,7 +353,7 @@ __device__ __forceinline__ void amg_serial_sums(double (&v)[S], const double* pr
 // streamed once for all of them); slots that terminate keep iterating with
 // alpha = beta = 0 (their vectors stay put) until the whole group is done.
 template <int S>
-__global__ void __launch_bounds__(AMG_T, 2) pcgamg2d_kernel(const PcgAmgParams prm) {
+__global__ void __launch_bounds__(AMG_T, AMG_MINB) pcgamg2d_kernel(const PcgAmgParams prm) {
   constexpr int NW = AMG_T / 32;
   extern __shared__ double sdense[];  // dense_n * S
   __shared__ double red[S][NW];
