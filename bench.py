@@ -54,6 +54,7 @@ sys.path.insert(0, ROOT)
 METRIC = "MC samples solved/sec (fp64 batched PCG) at 1 B200; % roofline; mean PCG iters"
 UNIT = "samples/s"
 FLOPS_PER_ROW_ITER = 31  # 1-D PCG iteration = 31 n flops
+AMG_VECTORS = 24  # per-sample vector passes of one AMG-preconditioned PCG iteration
 
 
 def parse():
@@ -84,6 +85,7 @@ def workload(cfg, B, K):
         r = cfg["mesh_resolution"]
         model = f"2-D P1 FEM on a {r}x{r} right-triangle mesh, {n} unknowns"
         pc = ("IC(0)" if cfg.get("precond") == "ic0"
+              else "SA-AMG V-cycle (the reference's default kind)" if cfg.get("precond") == "amg"
               else f"RCM + envelope Cholesky, {chol_rhs()} same-label samples per factor pass")
         kap = B * (r + 1) ** 2 * 8
     solve = f", PCG on the first {sub} samples" if sub else ""
@@ -262,6 +264,17 @@ def roofline(cfg, prof, total_iters, B, steps, device):
                                f"envelope factor (nnz(L) = {nnz}) streamed forward and backward once per S = {S} "
                                f"same-label right-hand sides, plus the IC(0) path's vector traffic",
                 "ms_per_launch": ms}
+    if kind == "pcg" and cfg["dim"] == 2 and cfg.get("precond") == "amg":
+        work = 8.0 * AMG_VECTORS * n * total_iters / lps
+        peak = measured_peaks().get("hbm_gbs")
+        achieved = work / (ms / 1e3) / 1e9
+        return {"kernel": "pcgamg2d", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if peak else None, "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, this pool's B200s)",
+                "algorithmic": f"8 x {AMG_VECTORS} n bytes per PCG iteration x sum of J: the per-sample vector passes "
+                               f"(PCG 15 n, V-cycle level 0 9 n); the centroid hierarchy is shared by a bucket's "
+                               f"samples and not counted",
+                "ms_per_launch": ms}
     if kind == "pcg" and cfg["dim"] == 2:
         work = 8.0 * (2 * npts + 14 * n) * total_iters / lps
         peak = measured_peaks().get("hbm_gbs")
@@ -329,6 +342,8 @@ def kernel_rooflines(cfg, prof, total_iters, B, K, steps, peaks):
     work = {}
     if cfg["dim"] == 1:
         work["pcg"] = (31.0 * n * total_iters / 1e12, "TFLOP/s", "fp64")
+    elif cfg.get("precond") == "amg":
+        work["pcg"] = (8.0 * AMG_VECTORS * n * total_iters / 1e9, "GB/s", "hbm")
     elif cfg.get("precond") == "cholesky":
         work["pcg"] = ((16.0 * cfg["_factor_entries"] / chol_rhs() + 8.0 * (2 * npts + 14 * n)) * total_iters / 1e9,
                        "GB/s", "hbm")
