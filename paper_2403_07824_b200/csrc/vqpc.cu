@@ -29,6 +29,7 @@
 #include "pcg1d.cuh"
 #include "pcg1d_exact.cuh"
 #include "pcg2d.cuh"
+#include "pcg2d_pair.cuh"
 #include "pcgamg2d.cuh"
 #include "pcgchol2d.cuh"
 #include "realise.cuh"
@@ -574,6 +575,28 @@ void run_pcgamg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t
   }
 }
 
+// the per-grid wavefront map (level | row << 16) and, when the mesh's b is not
+// uniform, the per-node right-hand side (shared by every sample)
+void ensure_gmap_bvec(vqpc_ctx* c, const double* d_kappa) {
+  if (!c->gmap.p) {
+    c->gmap.ensure(c->n);
+    build_gmap_kernel<<<64, P2_T, 0, c->stream>>>(c->g2, c->gmap.p);
+    launch_check(c);
+  }
+  if (!c->b2_checked) {  // is b_i = area_sum_i / 3 the same for every node? (yes when h = 1/r is exact)
+    c->bvec2.ensure(c->n);
+    // b does not depend on kappa; any coefficient row serves the assembly call
+    build_bvec_kernel<<<64, P2_T, 0, c->stream>>>(c->g2, c->kappa_c.p ? c->kappa_c.p : d_kappa, c->gmap.p,
+                                                  c->bvec2.p);
+    launch_check(c);
+    std::vector<double> hb(c->n);
+    CK(cudaMemcpyAsync(hb.data(), c->bvec2.p, sizeof(double) * c->n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->b2_uniform = std::all_of(hb.begin(), hb.end(), [&](double v) { return v == hb[0]; });
+    c->b2_checked = true;
+  }
+}
+
 void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d_kflag, const int32_t* d_perm,
                const int32_t* d_labels, int64_t B, int64_t out_base, double eps, int max_iter, const int32_t* d_mia,
                int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x, int64_t solve_limit) {
@@ -586,6 +609,62 @@ void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d
     run_pcgamg2d(c, d_kappa, ldk, d_kflag, d_perm, d_labels, B, out_base, eps, max_iter, d_mia, d_iters, d_rel,
                  d_status, d_x, solve_limit);
     return;
+  }
+  // two same-label samples per CTA (pcg2d_pair.cuh) unless VQPC_P2_PAIR=0
+  const char* pe = getenv("VQPC_P2_PAIR");
+  const bool pair = !(pe && atoi(pe) == 0);
+  if (pair) {
+    const int P = c->pb.P;
+    void (*pk)(const Pcg2dParams) = c->g2.m == 255 ? pcg2d_pair_kernel<255> : pcg2d_pair_kernel<0>;
+    CK(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P2P_DSMEM)));
+    int psm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&psm, pk, P2_T, P2P_DSMEM));
+    if (psm >= 1) {
+      c->ch_perm.ensure(B);
+      c->ch_off.ensure(P + 2);
+      c->ch_groups.ensure(B + P + 1);
+      c->ch_ngroups.ensure(1);
+      {
+        Timed tm(c, VQPC_K_BUCKET);
+        counting_sort(c, d_labels, d_perm, B, P, c->ch_perm.p, c->ch_off.p);
+        chol_groups_kernel<<<1, CG_T, 0, c->stream>>>(c->ch_off.p, P, 2, c->ch_groups.p, c->ch_ngroups.p);
+        launch_check(c);
+      }
+      const int64_t blocks = cap_groups(std::min<int64_t>(ceil_div(B, 2) + P + 1, static_cast<int64_t>(psm) * c->sm_count));
+      c->work2.ensure(static_cast<size_t>(blocks) * 2 * P2_WORK * c->n);
+      c->counter.ensure(1);
+      CK(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->stream));
+      Pcg2dParams prm{};
+      prm.g = c->g2;
+      prm.kappa = d_kappa;
+      prm.ldk = ldk;
+      prm.kflag = d_kflag;
+      prm.perm = c->ch_perm.p;
+      prm.labels = d_labels;
+      prm.groups = c->ch_groups.p;
+      prm.ngroups = c->ch_ngroups.p;
+      prm.fac = c->fac2.p;
+      prm.work = c->work2.p;
+      prm.B = B;
+      prm.out_base = out_base;
+      prm.solve_limit = solve_limit;
+      prm.eps = eps;
+      prm.max_iter = max_iter;
+      prm.max_iter_arr = d_mia;
+      prm.counter = c->counter.p;
+      prm.iters = d_iters;
+      prm.rel = d_rel;
+      prm.status = d_status;
+      prm.x_out = d_x;
+      prm.exact = c->exact;
+      ensure_gmap_bvec(c, d_kappa);
+      prm.gmap = c->gmap.p;
+      prm.bvec = c->b2_uniform ? nullptr : c->bvec2.p;
+      Timed tm(c, VQPC_K_PCG);
+      pk<<<static_cast<unsigned>(blocks), P2_T, P2P_DSMEM, c->stream>>>(prm);
+      launch_check(c);
+      return;
+    }
   }
   int per_sm = 0;
   // C4's mesh (m = 255) has a specialised instantiation; other sizes take the generic one
@@ -618,24 +697,8 @@ void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d
   prm.status = d_status;
   prm.x_out = d_x;
   prm.exact = c->exact;
-  if (!c->gmap.p) {
-    c->gmap.ensure(c->n);
-    build_gmap_kernel<<<64, P2_T, 0, c->stream>>>(c->g2, c->gmap.p);
-    launch_check(c);
-  }
+  ensure_gmap_bvec(c, d_kappa);
   prm.gmap = c->gmap.p;
-  if (!c->b2_checked) {  // is b_i = area_sum_i / 3 the same for every node? (yes when h = 1/r is exact)
-    c->bvec2.ensure(c->n);
-    // b does not depend on kappa; any coefficient row serves the assembly call
-    build_bvec_kernel<<<64, P2_T, 0, c->stream>>>(c->g2, c->kappa_c.p ? c->kappa_c.p : d_kappa, c->gmap.p,
-                                                  c->bvec2.p);
-    launch_check(c);
-    std::vector<double> hb(c->n);
-    CK(cudaMemcpyAsync(hb.data(), c->bvec2.p, sizeof(double) * c->n, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    c->b2_uniform = std::all_of(hb.begin(), hb.end(), [&](double v) { return v == hb[0]; });
-    c->b2_checked = true;
-  }
   prm.bvec = c->b2_uniform ? nullptr : c->bvec2.p;
   Timed tm(c, VQPC_K_PCG);
   kern<<<static_cast<unsigned>(blocks), P2_T, P2_DSMEM, c->stream>>>(prm);
