@@ -610,9 +610,11 @@ void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d
                  d_status, d_x, solve_limit);
     return;
   }
-  // two same-label samples per CTA (pcg2d_pair.cuh) unless VQPC_P2_PAIR=0
+  // two same-label samples per CTA (pcg2d_pair.cuh) with VQPC_P2_PAIR=1: bit-identical records,
+  // but measured slower than one sample per CTA (367 vs 436 samples/s on 2,048 C4 samples,
+  // profiles/r02g_ab_pair_c4.log), so the one-sample kernel stays the default
   const char* pe = getenv("VQPC_P2_PAIR");
-  const bool pair = !(pe && atoi(pe) == 0);
+  const bool pair = pe && atoi(pe) != 0;
   if (pair) {
     const int P = c->pb.P;
     void (*pk)(const Pcg2dParams) = c->g2.m == 255 ? pcg2d_pair_kernel<255> : pcg2d_pair_kernel<0>;
