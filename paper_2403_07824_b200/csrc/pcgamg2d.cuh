@@ -54,6 +54,13 @@ struct AmgLevelD {
   AmgEll A, P, Pt;
   const double* inv_diag;
   int voff;                 // levels >= 1: offset of (r, x, o) in the per-CTA coarse scratch
+  // level 0 of a structured mesh: the centroid matrix as its stencil (S, W, diagonal per
+  // row; row i's E / N couplings are the W of i + 1 / the S of i + m, bitwise equal), so
+  // the two level-0 A passes stream instead of gathering through the ELL columns. The
+  // reference's stored SW / NE zeros are skipped: r_i - (+-0) and a sum started at +0
+  // plus (+-0) are unchanged (the V-cycle's r is never -0), so the bits are the ELL path's.
+  const double *st_s, *st_w, *st_c;
+  int st_m;
 };
 
 struct AmgHierD {
@@ -102,6 +109,20 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
         x[i * S + s] = __dmul_rn(omega, __dmul_rn(di, acc[s]));
       }
       // res = r; res -= A x (Eigen's rewrite of `r - A x`), x_c recomputed with its owner's operations
+      if (L.st_c) {  // level 0, structured: CSR column order S, W, C, E, N
+        const int m = L.st_m, ix = i % m, iy = i / m;
+        auto sub = [&](double a, int c) {
+          const double dc = __ldg(L.inv_diag + c);
+#pragma unroll
+          for (int s = 0; s < S; ++s)
+            acc[s] = __dsub_rn(acc[s], __dmul_rn(a, __dmul_rn(omega, __dmul_rn(dc, r[c * S + s]))));
+        };
+        if (iy > 0) sub(__ldg(L.st_s + i), i - m);
+        if (ix > 0) sub(__ldg(L.st_w + i), i - 1);
+        sub(__ldg(L.st_c + i), i);
+        if (ix < m - 1) sub(__ldg(L.st_w + i + 1), i + 1);
+        if (iy < m - 1) sub(__ldg(L.st_s + i + m), i + m);
+      } else {
       int w;
       int e = ell_row(L.A, i, w);
       #pragma unroll 4
@@ -112,6 +133,7 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
 #pragma unroll
         for (int s = 0; s < S; ++s)
           acc[s] = __dsub_rn(acc[s], __dmul_rn(a, __dmul_rn(omega, __dmul_rn(dc, r[c * S + s]))));
+      }
       }
 #pragma unroll
       for (int s = 0; s < S; ++s) res[i * S + s] = acc[s];
@@ -256,6 +278,18 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
       double acc[S];
 #pragma unroll
       for (int s = 0; s < S; ++s) acc[s] = 0.0;
+      if (L.st_c) {  // level 0, structured: 0 + S, W, C, E, N products
+        const int m = L.st_m, ix = i % m, iy = i / m;
+        auto add = [&](double a, int c) {
+#pragma unroll
+          for (int s = 0; s < S; ++s) acc[s] = __dadd_rn(acc[s], __dmul_rn(a, xs[c * S + s]));
+        };
+        if (iy > 0) add(__ldg(L.st_s + i), i - m);
+        if (ix > 0) add(__ldg(L.st_w + i), i - 1);
+        add(__ldg(L.st_c + i), i);
+        if (ix < m - 1) add(__ldg(L.st_w + i + 1), i + 1);
+        if (iy < m - 1) add(__ldg(L.st_s + i + m), i + m);
+      } else {
       int w;
       int e = ell_row(L.A, i, w);
       #pragma unroll 4
@@ -265,6 +299,7 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
         const double a = __ldg(L.A.val + e);
 #pragma unroll
         for (int s = 0; s < S; ++s) acc[s] = __dadd_rn(acc[s], __dmul_rn(a, xs[c * S + s]));
+      }
       }
       const double di = __ldg(L.inv_diag + i);
 #pragma unroll

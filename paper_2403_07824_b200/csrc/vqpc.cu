@@ -1118,7 +1118,7 @@ void setup_amg(vqpc_ctx* c, const double* d_kc, int64_t ldk, int P) {
       }
     return o;
   };
-  struct LevOff { EllOff A, P, Pt; size_t inv; };
+  struct LevOff { EllOff A, P, Pt; size_t inv, st; };
   std::vector<std::vector<LevOff>> lo(P);
   std::vector<size_t> loff(P);
   std::vector<AmgHierD> hh(P);
@@ -1140,6 +1140,19 @@ void setup_amg(vqpc_ctx* c, const double* d_kc, int64_t ldk, int P) {
       }
       o.inv = hd.size();
       hd.insert(hd.end(), L.inv_diag.begin(), L.inv_diag.end());
+      o.st = SIZE_MAX;
+      if (l == 0) {  // the centroid matrix's stencil: S, W, diagonal per row (zeros where absent)
+        o.st = hd.size();
+        hd.resize(hd.size() + 3 * static_cast<size_t>(n), 0.0);
+        double* st = hd.data() + o.st;
+        for (int i = 0; i < n; ++i)
+          for (int e = L.A.ptr[i]; e < L.A.ptr[i + 1]; ++e) {
+            const int j = L.A.idx[e];
+            if (j == i - m) st[i] = L.A.val[e];
+            else if (j == i - 1) st[n + i] = L.A.val[e];
+            else if (j == i) st[2 * static_cast<size_t>(n) + i] = L.A.val[e];
+          }
+      }
       lo[p].push_back(o);
       AmgLevelD& d = hh[p].lv[l];
       d.n = L.A.rows;
@@ -1170,6 +1183,13 @@ void setup_amg(vqpc_ctx* c, const double* d_kc, int64_t ldk, int P) {
         d.Pt = ell_ptr(lo[p][l].Pt, d.nc, d.n);
       }
       d.inv_diag = c->amg_d.p + lo[p][l].inv;
+      d.st_s = d.st_w = d.st_c = nullptr;
+      d.st_m = m;
+      if (lo[p][l].st != SIZE_MAX) {
+        d.st_s = c->amg_d.p + lo[p][l].st;
+        d.st_w = d.st_s + n;
+        d.st_c = d.st_w + n;
+      }
     }
     hh[p].L = c->amg_d.p + loff[p];
   }
