@@ -670,7 +670,9 @@ void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d
   }
   int per_sm = 0;
   // C4's mesh (m = 255) has a specialised instantiation; other sizes take the generic one
-  void (*kern)(const Pcg2dParams) = c->g2.m == 255 ? pcg2d_kernel<255> : pcg2d_kernel<0>;
+  const char* ge = getenv("VQPC_P2_GENERIC");  // tests: the generic instantiation on C4's mesh
+  const bool spec = c->g2.m == 255 && !(ge && atoi(ge));
+  void (*kern)(const Pcg2dParams) = spec ? pcg2d_kernel<255> : pcg2d_kernel<0>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P2_DSMEM)));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P2_T, P2_DSMEM));
   if (per_sm < 1) throw ApiError{VQPC_CUDA_ERROR, "pcg2d kernel does not fit on an SM"};
