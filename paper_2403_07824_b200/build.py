@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.environ.get("VQPC_LIB", os.path.join(HERE, "libvqpc.so"))
 SOURCES = ["vqpc.cu", "host_quantizer.cu", "klbasis.cu"]
-HEADERS = ["amg_setup.cuh", "pcgamg2d.cuh", "pcg2d_pair.cuh", "common.cuh", "realise.cuh", "assign.cuh", "bucket.cuh", "factor.cuh", "pcg1d.cuh", "pcg1d_exact.cuh", "pcg2d.cuh", "pcgchol2d.cuh"]
+HEADERS = ["amg_setup.cuh", "pcgamg2d.cuh", "common.cuh", "realise.cuh", "assign.cuh", "bucket.cuh", "factor.cuh", "pcg1d.cuh", "pcg1d_exact.cuh", "pcg2d.cuh", "pcgchol2d.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 EXTRA = os.environ.get("VQPC_NVCC_FLAGS", "").split()

@@ -38,9 +38,10 @@
 
 namespace vqpc {
 
-constexpr int P2_T = 256;            // threads per CTA (one per grid row, r <= 257)
+constexpr int P2_T = 256;            // threads per CTA, one per grid row (r <= 257: two CTAs per SM)
+constexpr int P2_TBIG = 512;         // the same kernels with 512 threads, one CTA per SM (257 < r <= 513)
 constexpr int P2_FAC = 4;            // factor vectors per centroid: D, aW, aS, RN(1/D)
-constexpr int P2_MAXL = 2 * P2_T;    // max levels (2m - 1 <= 511)
+constexpr int P2_MAXL = 2 * P2_TBIG;  // max levels (2m - 1 <= 1023)
 
 // Order in which the reference's SparseBuilder sums a row's six diagonal
 // contributions (fem.cpp:177-211: std::sort by column, then duplicates summed in
@@ -240,10 +241,11 @@ __device__ __forceinline__ double div_by_pivot(double x, double d, double r) {
 
 // ---- (e) IC(0) factor of every centroid matrix (one CTA per centroid) ---------
 // fac layout per centroid (P2_FAC n doubles, wavefront order): D, aW, aS of A_c, RN(1/D).
-__global__ void __launch_bounds__(P2_T) factor2d_kernel(const double* kappa_c, int64_t ldk, int P, const Grid2D g,
+template <int TT>
+__global__ void __launch_bounds__(TT) factor2d_kernel(const double* kappa_c, int64_t ldk, int P, const Grid2D g,
                                                          double* fac, int* err) {
   __shared__ LevelTab tab;
-  __shared__ double dprev[2][P2_T + 1];
+  __shared__ double dprev[2][TT + 1];
   build_levels(tab, g);
   const int p = blockIdx.x, t = threadIdx.x;
   if (p >= P) return;
@@ -252,7 +254,7 @@ __global__ void __launch_bounds__(P2_T) factor2d_kernel(const double* kappa_c, i
   double* W = D + g.n;
   double* S = W + g.n;
   double* R = S + g.n;
-  for (int k = t; k <= P2_T; k += blockDim.x) dprev[0][k] = dprev[1][k] = 1.0;
+  for (int k = t; k <= TT; k += blockDim.x) dprev[0][k] = dprev[1][k] = 1.0;
   __syncthreads();
   bool ok = true;
   for (int l = 0; l < g.L; ++l) {
@@ -312,19 +314,21 @@ constexpr int P2_DEPTH = 6;
 constexpr int P2_DEPTH = P2_DEPTH_OVERRIDE;
 #endif  // cp.async prefetch ring depth (levels) for the IC(0) sweeps
 constexpr int P2_NOPS = 6;   // operands per node in the ring
-// Flat passes (P1, P2) stream the wavefront array in chunks of P2_T addresses:
+// Flat passes (P1, P2) stream the wavefront array in chunks of TT addresses:
 // each thread prefetches its own address of chunk k + P2_SD with cp.async into
 // a raw slot only it reads, and publishes the vector values its neighbours need
 // into 4-slot exchange rings (a node's neighbours lie in chunks k-1..k+1 since a
-// level holds <= P2_T - 1 nodes). One barrier per chunk.
+// level holds <= TT nodes). One barrier per chunk.
 constexpr int P2_SD = 3;       // chunks in flight
 constexpr int P2_RSLOT = P2_SD + 1;  // raw slots: the slot refilled in step k is the one read in step k-1
 constexpr int P2_RAW = 6;      // raw double vectors per address
 constexpr int P2_XCH = 4;      // exchange rings: p (or p_new), x_new, aW, aS; 4 chunk slots each (k-2..k+1 live)
-constexpr size_t P2_RING_SM = sizeof(double) * P2_DEPTH * P2_NOPS * P2_T;
-constexpr size_t P2_FLAT_SM = sizeof(double) * (P2_RSLOT * P2_RAW + 4 * P2_XCH) * P2_T + sizeof(int) * P2_RSLOT * P2_T;
-constexpr size_t P2_DSMEM = P2_RING_SM > P2_FLAT_SM ? P2_RING_SM : P2_FLAT_SM;
-static_assert(P2_T == 256, "chunk indexing assumes 256-address chunks");
+// dynamic shared memory of pcg2d_kernel<MC, TT>: the larger of the sweeps' ring and the flat passes' slots
+constexpr size_t p2_dsmem(int tt) {
+  const size_t ring = sizeof(double) * P2_DEPTH * P2_NOPS * tt;
+  const size_t flat = sizeof(double) * (P2_RSLOT * P2_RAW + 4 * P2_XCH) * tt + sizeof(int) * P2_RSLOT * tt;
+  return ring > flat ? ring : flat;
+}
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -395,15 +399,16 @@ __device__ __forceinline__ double serial_sum2d(const double* prod, int n, double
 
 // MC > 0 compiles the kernel for a fixed interior size m = MC (BASELINE C4: 255):
 // every vector offset j*n becomes an immediate and the level arithmetic folds.
-template <int MC>
-__global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
-  constexpr int NW = P2_T / 32;
+template <int MC, int TT>
+__global__ void __launch_bounds__(TT, TT == TT ? 2 : 1) pcg2d_kernel(const Pcg2dParams prm) {
+  constexpr int NW = TT / 32;
   extern __shared__ __align__(16) double dsm[];
-  __shared__ double sbuf[2][P2_T + 2];  // previous level of the running sweep (index iy + 1)
-  __shared__ int2 lvl_dd[P2_MAXL];       // per level: a - a_W, a_E - a
+  __shared__ double sbuf[2][TT + 2];  // previous level of the running sweep (index iy + 1)
+  __shared__ int2 lvl_dd[2 * TT];         // per level: a - a_W, a_E - a
   __shared__ double red[4][NW];
   __shared__ int64_t s_item;
   __shared__ double s_bval;
+  static_assert((TT & (TT - 1)) == 0, "the exchange rings index addresses modulo 4 TT");
   Grid2D g = prm.g;
   if constexpr (MC > 0) {
     g.m = MC;
@@ -411,7 +416,7 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
     g.L = 2 * MC - 1;
   }
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  for (int l = t; l < g.L; l += P2_T) lvl_dd[l] = make_int2(l > 0 ? wf_dw(l, g.m) : 0, l + 1 < g.L ? wf_de(l, g.m) : 0);
+  for (int l = t; l < g.L; l += TT) lvl_dd[l] = make_int2(l > 0 ? wf_dw(l, g.m) : 0, l + 1 < g.L ? wf_de(l, g.m) : 0);
   __syncthreads();
   const int n = g.n;
   double* base = prm.work + static_cast<size_t>(blockIdx.x) * P2_WORK * n;
@@ -483,7 +488,7 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
     // cp.async into a shared-memory ring (no registers held; a thread only reads
     // what it copied, so the ring needs no barrier), hiding the HBM latency that
     // otherwise stalls every one of the 2 x (2m-1) dependent levels.
-    double (*ring)[P2_NOPS][P2_T] = reinterpret_cast<double (*)[P2_NOPS][P2_T]>(dsm);
+    double (*ring)[P2_NOPS][TT] = reinterpret_cast<double (*)[P2_NOPS][TT]>(dsm);
     // Per-thread address cursors (no per-level table lookups): lin(l) is the
     // wavefront address of row t on level l (linear in t, valid or not), up(l) =
     // lin(l+1) - lin(l); row t has a node on level l iff 0 <= l - t < m.
@@ -499,7 +504,7 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
     // ring slots as 32-bit shared addresses; slot counters instead of l % depth
     const unsigned ring_sa = static_cast<unsigned>(__cvta_generic_to_shared(dsm)) + t * 8u;
     const unsigned long long pol_fac = l2_policy_last();
-    constexpr unsigned OPB = P2_T * 8u, SLOTB = P2_NOPS * P2_T * 8u;
+    constexpr unsigned OPB = TT * 8u, SLOTB = P2_NOPS * TT * 8u;
     auto next_slot = [](int sl) { return sl + 1 == P2_DEPTH ? 0 : sl + 1; };
     auto fwd_issue = [&](int l, int a, int sl) {
       if (on(l)) {
@@ -544,9 +549,9 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
         if (on(l)) {
           const double* op = &ring[sc][0][t];
           double v = op[0];
-          if (l - t > 0) v = __dsub_rn(v, __dmul_rn(op[P2_T], sbuf[prv][t + 1]));
-          if (t > 0) v = __dsub_rn(v, __dmul_rn(op[2 * P2_T], sbuf[prv][t]));
-          v = div_by_pivot(v, op[3 * P2_T], op[4 * P2_T]);
+          if (l - t > 0) v = __dsub_rn(v, __dmul_rn(op[TT], sbuf[prv][t + 1]));
+          if (t > 0) v = __dsub_rn(v, __dmul_rn(op[2 * TT], sbuf[prv][t]));
+          v = div_by_pivot(v, op[3 * TT], op[4 * TT]);
           VQPC_DCHECK(ac >= 0 && ac < n);
           Y[ac] = v;
           sbuf[cur][t + 1] = v;
@@ -578,13 +583,13 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
           const double* op = &ring[sc][0][t];
           double acc = 0.0;
           if (l - t < m - 1) acc = __dadd_rn(acc, __dmul_rn(op[0], sbuf[prv][t + 1]));
-          if (t < m - 1) acc = __dadd_rn(acc, __dmul_rn(op[P2_T], sbuf[prv][t + 2]));
-          const double z = __dsub_rn(op[3 * P2_T], div_by_pivot(acc, op[2 * P2_T], op[5 * P2_T]));
+          if (t < m - 1) acc = __dadd_rn(acc, __dmul_rn(op[TT], sbuf[prv][t + 2]));
+          const double z = __dsub_rn(op[3 * TT], div_by_pivot(acc, op[2 * TT], op[5 * TT]));
           VQPC_DCHECK(ac >= 0 && ac < n);
           Z[ac] = z;
           sbuf[cur][t + 1] = z;
-          rz_part = fma(op[4 * P2_T], z, rz_part);
-          if (exact) Prod[t * m + (l - t)] = __dmul_rn(op[4 * P2_T], z);
+          rz_part = fma(op[4 * TT], z, rz_part);
+          if (exact) Prod[t * m + (l - t)] = __dmul_rn(op[4 * TT], z);
         }
         ac -= up(l - 1);
         sc = next_slot(sc);
@@ -610,16 +615,16 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
         const double* Po = Pb[pc];
         double* Pn = Pb[pc ^ 1];
         const bool first = j == 1;
-        const int NC = (n + P2_T - 1) / P2_T;
-        double* raw = dsm;                                   // [P2_RSLOT][P2_RAW][P2_T]
-        double* xch = dsm + P2_RSLOT * P2_RAW * P2_T;        // [P2_XCH][4][P2_T]
-        int* rawi = reinterpret_cast<int*>(xch + 4 * P2_XCH * P2_T);  // [P2_RSLOT][P2_T]
-        auto RAW = [&](int k, int v) -> double* { return raw + ((static_cast<unsigned>(k) % P2_RSLOT) * P2_RAW + v) * P2_T + t; };
+        const int NC = (n + TT - 1) / TT;
+        double* raw = dsm;                                   // [P2_RSLOT][P2_RAW][TT]
+        double* xch = dsm + P2_RSLOT * P2_RAW * TT;        // [P2_XCH][4][TT]
+        int* rawi = reinterpret_cast<int*>(xch + 4 * P2_XCH * TT);  // [P2_RSLOT][TT]
+        auto RAW = [&](int k, int v) -> double* { return raw + ((static_cast<unsigned>(k) % P2_RSLOT) * P2_RAW + v) * TT + t; };
         // chunk slot (q >> 8) & 3, column q & 255: together q & 1023
-        auto XCH = [&](int x, int q) -> double& { return xch[x * 4 * P2_T + (q & (4 * P2_T - 1))]; };
+        auto XCH = [&](int x, int q) -> double& { return xch[x * 4 * TT + (q & (4 * TT - 1))]; };
         const unsigned long long pol_str = l2_policy_first();
         auto flat_issue = [&](int k, const double* v0, const double* v1, const double* v2) {
-          const int a = k * P2_T + t;
+          const int a = k * TT + t;
           if (k < NC && a < n) {
             if (v0) cp_async8p(RAW(k, 0), v0 + a, pol_str);
             if (v1) cp_async8p(RAW(k, 1), v1 + a, pol_str);
@@ -627,7 +632,7 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
             cp_async8p(RAW(k, 3), As + a, pol_str);
             cp_async8p(RAW(k, 4), Aw + a, pol_str);
             cp_async8p(RAW(k, 5), Ad + a, pol_str);
-            cp_async4(rawi + (static_cast<unsigned>(k) % P2_RSLOT) * P2_T + t, prm.gmap + a);
+            cp_async4(rawi + (static_cast<unsigned>(k) % P2_RSLOT) * TT + t, prm.gmap + a);
           }
           cp_commit();
         };
@@ -657,14 +662,14 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
             const int plv = clv;
             if (k < NC) {
               cp_wait<P2_SD - 1>();
-              const int a = k * P2_T + t;
+              const int a = k * TT + t;
               if (a < n) {
                 const double z = *RAW(k, 0);
                 const double pcv = first ? z : __dadd_rn(z, __dmul_rn(beta, *RAW(k, 1)));
                 cs = *RAW(k, 3);
                 cw = *RAW(k, 4);
                 cd = *RAW(k, 5);
-                clv = rawi[(static_cast<unsigned>(k) % P2_RSLOT) * P2_T + t];
+                clv = rawi[(static_cast<unsigned>(k) % P2_RSLOT) * TT + t];
                 XCH(0, a) = pcv;
                 XCH(2, a) = cw;
                 XCH(3, a) = cs;
@@ -673,7 +678,7 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
             }
             flat_issue(k + P2_SD, Z, first ? nullptr : Po, nullptr);
             __syncthreads();
-            const int a = (k - 1) * P2_T + t;
+            const int a = (k - 1) * TT + t;
             if (k >= 1 && a < n) {
               const Nb b = nbrs(a, plv);
               const double pcv = XCH(0, a);
@@ -710,7 +715,7 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
             const int plv = clv;
             if (k < NC) {
               cp_wait<P2_SD - 1>();
-              const int a = k * P2_T + t;
+              const int a = k * TT + t;
               if (a < n) {
                 if (prm.bvec) cb = __ldg(prm.bvec + a);  // consumed one chunk later (latency hidden)
                 const double pvv = *RAW(k, 0);
@@ -719,7 +724,7 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
                 cs = *RAW(k, 3);
                 cw = *RAW(k, 4);
                 cd = *RAW(k, 5);
-                clv = rawi[(static_cast<unsigned>(k) % P2_RSLOT) * P2_T + t];
+                clv = rawi[(static_cast<unsigned>(k) % P2_RSLOT) * TT + t];
                 XCH(0, a) = pvv;
                 XCH(1, a) = xn;
                 XCH(2, a) = cw;
@@ -729,7 +734,7 @@ __global__ void __launch_bounds__(P2_T, 2) pcg2d_kernel(const Pcg2dParams prm) {
             }
             flat_issue(k + P2_SD, Pv, Xo, Rv);
             __syncthreads();
-            const int a = (k - 1) * P2_T + t;
+            const int a = (k - 1) * TT + t;
             if (k >= 1 && a < n) {
               const Nb b = nbrs(a, plv);
               const double aE = xv(2, b.e), aN = xv(3, b.nn);
@@ -802,10 +807,11 @@ __global__ void __launch_bounds__(P2_T) build_bvec_kernel(const Grid2D g, const 
 }
 
 // natural-order IC(0) apply for one vector (parity tests), single CTA
-__global__ void __launch_bounds__(P2_T) precond2d_apply_kernel(const double* fac, int p, const Grid2D g,
+template <int TT>
+__global__ void __launch_bounds__(TT) precond2d_apply_kernel(const double* fac, int p, const Grid2D g,
                                                                 const double* r_nat, double* z_nat, double* ws) {
   __shared__ LevelTab tab;
-  __shared__ double sbuf[2][P2_T + 2];
+  __shared__ double sbuf[2][TT + 2];
   build_levels(tab, g);
   const int t = threadIdx.x, n = g.n;
   const double* FD = fac + static_cast<size_t>(p) * P2_FAC * n;
@@ -813,7 +819,7 @@ __global__ void __launch_bounds__(P2_T) precond2d_apply_kernel(const double* fac
   const double* FS = FW + n;
   double* Y = ws;
   sbuf[0][t + 1] = sbuf[1][t + 1] = 0.0;
-  if (t == 0) sbuf[0][0] = sbuf[1][0] = sbuf[0][P2_T + 1] = sbuf[1][P2_T + 1] = 0.0;
+  if (t == 0) sbuf[0][0] = sbuf[1][0] = sbuf[0][TT + 1] = sbuf[1][TT + 1] = 0.0;
   __syncthreads();
   for (int l = 0; l < g.L; ++l) {
     const int cur = l & 1, prv = cur ^ 1;

@@ -29,7 +29,6 @@
 #include "pcg1d.cuh"
 #include "pcg1d_exact.cuh"
 #include "pcg2d.cuh"
-#include "pcg2d_pair.cuh"
 #include "pcgamg2d.cuh"
 #include "pcgchol2d.cuh"
 #include "realise.cuh"
@@ -610,71 +609,18 @@ void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d
                  d_status, d_x, solve_limit);
     return;
   }
-  // two same-label samples per CTA (pcg2d_pair.cuh) with VQPC_P2_PAIR=1: bit-identical records,
-  // but measured slower than one sample per CTA (367 vs 436 samples/s on 2,048 C4 samples,
-  // profiles/r02g_ab_pair_c4.log), so the one-sample kernel stays the default
-  const char* pe = getenv("VQPC_P2_PAIR");
-  const bool pair = pe && atoi(pe) != 0;
-  if (pair) {
-    const int P = c->pb.P;
-    void (*pk)(const Pcg2dParams) = c->g2.m == 255 ? pcg2d_pair_kernel<255> : pcg2d_pair_kernel<0>;
-    CK(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P2P_DSMEM)));
-    int psm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&psm, pk, P2_T, P2P_DSMEM));
-    if (psm >= 1) {
-      c->ch_perm.ensure(B);
-      c->ch_off.ensure(P + 2);
-      c->ch_groups.ensure(B + P + 1);
-      c->ch_ngroups.ensure(1);
-      {
-        Timed tm(c, VQPC_K_BUCKET);
-        counting_sort(c, d_labels, d_perm, B, P, c->ch_perm.p, c->ch_off.p);
-        chol_groups_kernel<<<1, CG_T, 0, c->stream>>>(c->ch_off.p, P, 2, c->ch_groups.p, c->ch_ngroups.p);
-        launch_check(c);
-      }
-      const int64_t blocks = cap_groups(std::min<int64_t>(ceil_div(B, 2) + P + 1, static_cast<int64_t>(psm) * c->sm_count));
-      c->work2.ensure(static_cast<size_t>(blocks) * 2 * P2_WORK * c->n);
-      c->counter.ensure(1);
-      CK(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->stream));
-      Pcg2dParams prm{};
-      prm.g = c->g2;
-      prm.kappa = d_kappa;
-      prm.ldk = ldk;
-      prm.kflag = d_kflag;
-      prm.perm = c->ch_perm.p;
-      prm.labels = d_labels;
-      prm.groups = c->ch_groups.p;
-      prm.ngroups = c->ch_ngroups.p;
-      prm.fac = c->fac2.p;
-      prm.work = c->work2.p;
-      prm.B = B;
-      prm.out_base = out_base;
-      prm.solve_limit = solve_limit;
-      prm.eps = eps;
-      prm.max_iter = max_iter;
-      prm.max_iter_arr = d_mia;
-      prm.counter = c->counter.p;
-      prm.iters = d_iters;
-      prm.rel = d_rel;
-      prm.status = d_status;
-      prm.x_out = d_x;
-      prm.exact = c->exact;
-      ensure_gmap_bvec(c, d_kappa);
-      prm.gmap = c->gmap.p;
-      prm.bvec = c->b2_uniform ? nullptr : c->bvec2.p;
-      Timed tm(c, VQPC_K_PCG);
-      pk<<<static_cast<unsigned>(blocks), P2_T, P2P_DSMEM, c->stream>>>(prm);
-      launch_check(c);
-      return;
-    }
-  }
   int per_sm = 0;
-  // C4's mesh (m = 255) has a specialised instantiation; other sizes take the generic one
+  // C4's mesh (m = 255) has a specialised instantiation; other sizes take the generic one.
+  // Meshes with more than 256 interior rows run the same kernel with 512 threads (one
+  // thread per grid row, one CTA per SM).
   const char* ge = getenv("VQPC_P2_GENERIC");  // tests: the generic instantiation on C4's mesh
   const bool spec = c->g2.m == 255 && !(ge && atoi(ge));
-  void (*kern)(const Pcg2dParams) = spec ? pcg2d_kernel<255> : pcg2d_kernel<0>;
+  const bool big = c->g2.m > P2_T;
+  const int TT = big ? P2_TBIG : P2_T;
+  void (*kern)(const Pcg2dParams) = big ? pcg2d_kernel<0, P2_TBIG> : spec ? pcg2d_kernel<255, P2_T> : pcg2d_kernel<0, P2_T>;
+  const size_t P2_DSMEM = p2_dsmem(TT);
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P2_DSMEM)));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P2_T, P2_DSMEM));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TT, P2_DSMEM));
   if (per_sm < 1) throw ApiError{VQPC_CUDA_ERROR, "pcg2d kernel does not fit on an SM"};
   const int64_t blocks = cap_groups(std::min<int64_t>(B, static_cast<int64_t>(per_sm) * c->sm_count));
   c->work2.ensure(static_cast<size_t>(blocks) * P2_WORK * c->n);
@@ -705,7 +651,7 @@ void run_pcg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t* d
   prm.gmap = c->gmap.p;
   prm.bvec = c->b2_uniform ? nullptr : c->bvec2.p;
   Timed tm(c, VQPC_K_PCG);
-  kern<<<static_cast<unsigned>(blocks), P2_T, P2_DSMEM, c->stream>>>(prm);
+  kern<<<static_cast<unsigned>(blocks), TT, P2_DSMEM, c->stream>>>(prm);
   launch_check(c);
 }
 
@@ -1236,7 +1182,10 @@ void factor_coefficients(vqpc_ctx* c, const double* d_kc, int64_t ldk, int P) {
     } else if (pb.dim == 2) {
       c->fac2.ensure(static_cast<size_t>(P) * P2_FAC * c->n);
       Timed tm(c, VQPC_K_OTHER);
-      factor2d_kernel<<<P, P2_T, 0, c->stream>>>(d_kc, ldk, P, c->g2, c->fac2.p, c->err.p);
+      if (c->g2.m > P2_T)
+        factor2d_kernel<P2_TBIG><<<P, P2_TBIG, 0, c->stream>>>(d_kc, ldk, P, c->g2, c->fac2.p, c->err.p);
+      else
+        factor2d_kernel<P2_T><<<P, P2_T, 0, c->stream>>>(d_kc, ldk, P, c->g2, c->fac2.p, c->err.p);
       launch_check(c);
     } else {
       c->fac.ensure(static_cast<size_t>(P) * c->NP);
@@ -1410,10 +1359,11 @@ int vqpc_ctx_create(const vqpc_problem* pb, vqpc_ctx** out) {
   const bool grid = pb->method == VQPC_GRID || pb->method == VQPC_SIGN_GRID;
   if (grid && !pb->latent) return VQPC_INVALID_CODEBOOK;
   if (pb->dim == 1 && pb->precond != VQPC_PC_CHOLESKY) return VQPC_INVALID_CONFIG;
-  // IC(0)'s level sweeps put one thread on each grid row (r - 1 <= 256); the cholesky
-  // kind checks its envelope width at setup; the AMG kind has no mesh-size limit
+  // IC(0)'s level sweeps put one thread on each grid row (r - 1 <= 512: 256-thread CTAs up
+  // to r = 257, 512-thread CTAs beyond); the cholesky kind checks its envelope width at
+  // setup; the AMG kind has no mesh-size limit
   if (pb->dim == 2 && ((pb->precond != VQPC_PC_IC0 && pb->precond != VQPC_PC_CHOLESKY && pb->precond != VQPC_PC_AMG) ||
-                       (pb->precond == VQPC_PC_IC0 && pb->size - 1 > P2_T)))
+                       (pb->precond == VQPC_PC_IC0 && pb->size - 1 > P2_TBIG)))
     return VQPC_INVALID_CONFIG;
   auto* c = new vqpc_ctx();
   c->pb = *pb;
@@ -1611,8 +1561,12 @@ int vqpc_precond_apply(vqpc_ctx* c, int p, const double* r, double* z) {
       cholapply_serial_kernel<<<1, 1, 0, c->stream>>>(c->ch_L.p, c->ch_ldL, c->clay, p, c->dvec.p,
                                                       c->dvec.p + 2 * c->n, c->dvec.p + c->n);
     else if (c->pb.dim == 2)
-      precond2d_apply_kernel<<<1, P2_T, 0, c->stream>>>(c->fac2.p, p, c->g2, c->dvec.p, c->dvec.p + c->n,
-                                                        c->dvec.p + 2 * c->n);
+      if (c->g2.m > P2_T)
+        precond2d_apply_kernel<P2_TBIG><<<1, P2_TBIG, 0, c->stream>>>(c->fac2.p, p, c->g2, c->dvec.p, c->dvec.p + c->n,
+                                                                      c->dvec.p + 2 * c->n);
+      else
+        precond2d_apply_kernel<P2_T><<<1, P2_T, 0, c->stream>>>(c->fac2.p, p, c->g2, c->dvec.p, c->dvec.p + c->n,
+                                                                c->dvec.p + 2 * c->n);
     else
       precond1d_apply_kernel<<<1, 1, 0, c->stream>>>(c->fac.p, c->NP, p, c->n, c->dvec.p, c->dvec.p + c->n);
     launch_check(c);

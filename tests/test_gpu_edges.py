@@ -114,17 +114,18 @@ def test_duplicate_rows_and_ragged_chunks():
 
 def test_size_limits():
     """n = 8192 rows is the largest 1-D system (2-CTA clusters; C5 has 8191); beyond it the
-    context refuses with invalid-config instead of failing at launch. 2-D
-    meshes above r = 257 likewise."""
+    context refuses with invalid-config instead of failing at launch. The 2-D
+    IC(0) kind puts one thread on each grid row: r <= 513 (512-thread CTAs above
+    r = 257), beyond it invalid-config likewise."""
     rng = np.random.default_rng(0)
     cb = dict(method="kmeans", map="scale", lambdas=np.ones(2), centroids=rng.standard_normal((4, 2)))
-    for dim, size in ((1, 8193), (2, 257)):
+    for dim, size in ((1, 8193), (2, 257), (2, 513)):
         nn = size if dim == 1 else (size + 1) ** 2
         basis = dict(eigenvalues=np.array([1.0, 0.5]), eigenvectors=rng.standard_normal((2, nn)) * 1e-3)
         ctx = lib.Context(dim, size, basis, cb, "cholesky" if dim == 1 else "ic0")
         ctx.factor_centroids()
         ctx.close()
-    for dim, size in ((1, 8194), (2, 258)):
+    for dim, size in ((1, 8194), (2, 514)):
         nn = size if dim == 1 else (size + 1) ** 2
         basis = dict(eigenvalues=np.array([1.0, 0.5]), eigenvectors=np.zeros((2, nn)))
         with pytest.raises(lib.VqpcError, match="invalid-config"):

@@ -146,3 +146,36 @@ def test_c4chol_full_size_64_samples():
     assert cmp["status_agree"] == 1.0 and cmp["n_both"] == 64
     assert cmp["max_dj"] <= max(2, yard["max_dj"]), (cmp, yard)
     assert cmp["mean_diff"] <= max(3 * yard["mean_diff"], 0.05), (cmp, yard)
+
+
+def test_ic0_paper_size_mesh():
+    """The paper's problem size (n = 99,681 unknowns) on the structured
+    mesh r = 317 (99,856 unknowns) with the IC(0) kind: meshes beyond r = 257 run the
+    level sweeps with 512-thread CTAs (one thread per grid row). Reference-order mode
+    is bit-identical to the oracle; the fast mode's J stays within the C4 band."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from tests.helpers import CONFIGS
+    name = "C4ic317"
+    CONFIGS.setdefault(name, campaign.scaled(campaign.CONFIGS["C4"], mesh_resolution=317, name=name))
+    cfg, basis, cb, xi = setup_case(name, 16)
+    ocb = oracle_codebook(cb)
+    ctx = campaign.make_context(cfg, dict(basis=basis, codebook=cb))
+    assert ctx.n == 316 * 316
+    fast = ctx.run_campaign(xi, cfg["eps"])
+    ctx.set_exact_reductions(True)
+    kc = ctx.centroid_coefficients()
+    labels = oracle.assign(ocb, xi)
+    assert np.array_equal(fast["labels"], labels)
+    kap, _ = ctx.realise(xi)
+    it, rel, st, x = ctx.solve_batch(xi, labels, cfg["eps"], want_x=True)
+    ctx.close()
+    pset = oracle.PreconditionerSet.from_coefficients(2, cfg["mesh_resolution"], "ic0", kc)
+    with ThreadPoolExecutor(THREADS) as ex:
+        outs = list(ex.map(lambda i: pset.pcg(int(labels[i]), kap[i], cfg["eps"]), range(len(xi))))
+    for i, out in enumerate(outs):
+        assert out["iterations"] == it[i] and out["status"] == st[i] and out["rel"] == rel[i], (i, out["iterations"], it[i])
+        assert np.array_equal(out["x"], x[i]), i
+    dj = np.abs(fast["iterations"].astype(int) - it)
+    print("r=317 (n=99,856) IC(0): J exact", it.tolist(), "fast", fast["iterations"].tolist(), flush=True)
+    assert (fast["status"] == 0).all() and dj.max() <= 20 and abs(fast["iterations"].mean() - it.mean()) <= 0.005 * it.mean()
