@@ -37,17 +37,19 @@ constexpr int kAmgRowU = AMG_ROWU;
 #define AMG_MINB 3                   // resident CTAs per SM the register budget targets (3: +12 % over 2, r02f A/B)
 #endif
 
-// Sliced ELL: rows in slices of 32; slice s holds width_s = (soff[s+1]-soff[s])/32
-// entries per row, entry k of row i at soff[s] + 32 k + (i & 31) for k < rlen[i]
-// (col -1 pads the rest). The row loops run to rlen[i] with no exit that depends on
-// a loaded column, so the unrolled iterations' loads issue together.
+// Sliced ELL: rows in slices of 32; slice s holds width_s entries per row, entry k of
+// row i at e0_i + 32 k for k < len_i, with row[i] = {e0_i, len_i} (e0_i = the slice's
+// offset + (i & 31)). An entry is one 16-byte record {value, column (low 32 bits of the
+// second word)}: one load per entry instead of a column and a value load, and one
+// 8-byte load per row for its offset and length. The row loops run to len_i with no exit
+// that depends on a loaded column, so the unrolled iterations' loads issue together,
+// and every loop fetches the next row's {e0, len} while it works on the current row.
 struct AmgEll {
-  const int* soff;
-  const int* col;
-  const double* val;
-  const int* rlen;          // stored entries of each row (the loops end there: no data-dependent exit)
+  const int2* row;          // per row: first record, stored entries
+  const double2* rec;       // records {val, col}
   int rows, cols;           // shape (bounds checks of the check build)
 };
+__device__ __forceinline__ int ell_col(const double2& rc) { return __double2loint(rc.y); }
 
 struct AmgLevelD {
   int n, nc;                // rows; rows of the next level (0 on the coarsest)
@@ -69,10 +71,9 @@ struct AmgHierD {
   AmgLevelD lv[AMG_MAXLEV];
 };
 
-__device__ __forceinline__ int ell_row(const AmgEll& M, int i, int& len) {
+__device__ __forceinline__ int2 ell_row(const AmgEll& M, int i) {
   VQPC_DCHECK(i >= 0 && i < M.rows);
-  len = __ldg(M.rlen + i);
-  return __ldg(M.soff + (i >> 5)) + (i & 31);
+  return __ldg(M.row + i);
 }
 
 // ---- one V-cycle z = M^{-1} r for S right-hand sides on hierarchy H ---------------
@@ -99,8 +100,12 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
     const double* __restrict__ r = vr(l);
     double* __restrict__ x = vx(l);
     double* __restrict__ res = vo(l);  // the residual; later this level's output
+    int2 rw_n = make_int2(0, 0);
+    if (!L.st_c && t < L.n) rw_n = ell_row(L.A, t);
 #pragma unroll kAmgRowU
     for (int i = t; i < L.n; i += AMG_T) {
+      const int2 rw = rw_n;
+      if (!L.st_c && i + AMG_T < L.n) rw_n = ell_row(L.A, i + AMG_T);
       const double di = __ldg(L.inv_diag + i);
       double acc[S];
 #pragma unroll
@@ -123,13 +128,14 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
         if (ix < m - 1) sub(__ldg(L.st_w + i + 1), i + 1);
         if (iy < m - 1) sub(__ldg(L.st_s + i + m), i + m);
       } else {
-      int w;
-      int e = ell_row(L.A, i, w);
+      const int w = rw.y;
+      int e = rw.x;
       #pragma unroll 4
       for (int k = 0; k < w; ++k, e += 32) {
-        const int c = __ldg(L.A.col + e);
-        VQPC_DCHECK(c < L.A.cols);
-        const double a = __ldg(L.A.val + e), dc = __ldg(L.inv_diag + c);
+        const double2 rc = __ldg(L.A.rec + e);
+        const int c = ell_col(rc);
+        VQPC_DCHECK(c >= 0 && c < L.A.cols);
+        const double a = rc.x, dc = __ldg(L.inv_diag + c);
 #pragma unroll
         for (int s = 0; s < S; ++s)
           acc[s] = __dsub_rn(acc[s], __dmul_rn(a, __dmul_rn(omega, __dmul_rn(dc, r[c * S + s]))));
@@ -141,18 +147,22 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
     __syncthreads();
     double* __restrict__ rn = vr(l + 1);
     const double* __restrict__ rs = res;
+    rw_n = t < L.nc ? ell_row(L.Pt, t) : make_int2(0, 0);
 #pragma unroll kAmgRowU
     for (int c = t; c < L.nc; c += AMG_T) {  // P^T residual: 0 + sum, ascending fine rows
+      const int2 rw = rw_n;
+      if (c + AMG_T < L.nc) rw_n = ell_row(L.Pt, c + AMG_T);
       double acc[S];
 #pragma unroll
       for (int s = 0; s < S; ++s) acc[s] = 0.0;
-      int w;
-      int e = ell_row(L.Pt, c, w);
+      const int w = rw.y;
+      int e = rw.x;
       #pragma unroll 4
       for (int k = 0; k < w; ++k, e += 32) {
-        const int q = __ldg(L.Pt.col + e);
-        VQPC_DCHECK(q < L.Pt.cols);
-        const double v = __ldg(L.Pt.val + e);
+        const double2 rc = __ldg(L.Pt.rec + e);
+        const int q = ell_col(rc);
+        VQPC_DCHECK(q >= 0 && q < L.Pt.cols);
+        const double v = rc.x;
 #pragma unroll
         for (int s = 0; s < S; ++s) acc[s] = __dadd_rn(acc[s], __dmul_rn(v, rs[q * S + s]));
       }
@@ -214,12 +224,14 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
         double acc[S];
 #pragma unroll
         for (int s = 0; s < S; ++s) acc[s] = 0.0;
-        int w;
-        int e = ell_row(L.A, i, w);
+        const int2 rw = ell_row(L.A, i);
+        const int w = rw.y;
+        int e = rw.x;
         #pragma unroll 4
         for (int k = 0; k < w; ++k, e += 32) {
-          const int c = __ldg(L.A.col + e);
-          const double a = __ldg(L.A.val + e);
+          const double2 rc = __ldg(L.A.rec + e);
+          const int c = ell_col(rc);
+          const double a = rc.x;
 #pragma unroll
           for (int s = 0; s < S; ++s) acc[s] = __dadd_rn(acc[s], __dmul_rn(a, x[c * S + s]));
         }
@@ -252,18 +264,22 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
     const double* __restrict__ r = vr(l);
     double* __restrict__ x = vx(l);
     const double* __restrict__ oc = vo(l + 1);
+    int2 rw_n = t < L.n ? ell_row(L.P, t) : make_int2(0, 0);
 #pragma unroll kAmgRowU
     for (int i = t; i < L.n; i += AMG_T) {  // x += P coarse (x_i + P_ik c_k, ascending k)
+      const int2 rw = rw_n;
+      if (i + AMG_T < L.n) rw_n = ell_row(L.P, i + AMG_T);
       double acc[S];
 #pragma unroll
       for (int s = 0; s < S; ++s) acc[s] = x[i * S + s];
-      int w;
-      int e = ell_row(L.P, i, w);
+      const int w = rw.y;
+      int e = rw.x;
       #pragma unroll 4
       for (int k = 0; k < w; ++k, e += 32) {
-        const int c = __ldg(L.P.col + e);
-        VQPC_DCHECK(c < L.P.cols);
-        const double v = __ldg(L.P.val + e);
+        const double2 rc = __ldg(L.P.rec + e);
+        const int c = ell_col(rc);
+        VQPC_DCHECK(c >= 0 && c < L.P.cols);
+        const double v = rc.x;
 #pragma unroll
         for (int s = 0; s < S; ++s) acc[s] = __dadd_rn(acc[s], __dmul_rn(v, oc[c * S + s]));
       }
@@ -273,8 +289,11 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
     __syncthreads();
     double* __restrict__ o = l == 0 ? z : vo(l);
     const double* __restrict__ xs = x;
+    rw_n = (!L.st_c && t < L.n) ? ell_row(L.A, t) : make_int2(0, 0);
 #pragma unroll kAmgRowU
     for (int i = t; i < L.n; i += AMG_T) {  // x += omega D^-1 (r - A x), A x into a fresh vector
+      const int2 rw = rw_n;
+      if (!L.st_c && i + AMG_T < L.n) rw_n = ell_row(L.A, i + AMG_T);
       double acc[S];
 #pragma unroll
       for (int s = 0; s < S; ++s) acc[s] = 0.0;
@@ -290,13 +309,14 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
         if (ix < m - 1) add(__ldg(L.st_w + i + 1), i + 1);
         if (iy < m - 1) add(__ldg(L.st_s + i + m), i + m);
       } else {
-      int w;
-      int e = ell_row(L.A, i, w);
+      const int w = rw.y;
+      int e = rw.x;
       #pragma unroll 4
       for (int k = 0; k < w; ++k, e += 32) {
-        const int c = __ldg(L.A.col + e);
-        VQPC_DCHECK(c < L.A.cols);
-        const double a = __ldg(L.A.val + e);
+        const double2 rc = __ldg(L.A.rec + e);
+        const int c = ell_col(rc);
+        VQPC_DCHECK(c >= 0 && c < L.A.cols);
+        const double a = rc.x;
 #pragma unroll
         for (int s = 0; s < S; ++s) acc[s] = __dadd_rn(acc[s], __dmul_rn(a, xs[c * S + s]));
       }

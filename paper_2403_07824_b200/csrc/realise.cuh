@@ -42,13 +42,22 @@ struct RealiseParams {
                            // 2 kappa == 0 (assembly's invalid-coefficient); nullable
 };
 
+// dynamic shared memory of realise_kernel: two stages of {W tile, Phi tile}
+constexpr int RL_STAGE = RL_BM * RL_WLD + RL_BK * RL_PLD;  // doubles per stage
+constexpr size_t RL_SMEM = sizeof(double) * 2 * RL_STAGE;
+
 static __global__ void __launch_bounds__(RL_THREADS) realise_kernel(const RealiseParams prm) {
-  __shared__ double sW[RL_BM * RL_WLD];
-  __shared__ double sP[RL_BK * RL_PLD];
+  // K blocks are double-buffered: the global loads of block k + 1 are issued into
+  // registers before the DMMA loop of block k and stored to the other stage after it,
+  // so their latency hides behind the tensor work and one barrier per block suffices.
+  // The accumulation order over k is unchanged (kappa bits as the single-stage kernel).
+  extern __shared__ __align__(16) double rl_smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps
   const int64_t b0 = static_cast<int64_t>(blockIdx.y) * RL_BM;
   const int i0 = blockIdx.x * RL_BN;
+  constexpr int NWE = RL_BM * RL_BK / RL_THREADS;  // W elements per thread (4)
+  constexpr int NPE = RL_BK * RL_BN / RL_THREADS;  // Phi elements per thread (8)
 
   double acc[4][4][2];
 #pragma unroll
@@ -56,26 +65,45 @@ static __global__ void __launch_bounds__(RL_THREADS) realise_kernel(const Realis
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
 
-  for (int k0 = 0; k0 < prm.K_use; k0 += RL_BK) {
-    __syncthreads();
-    // W tile: 64 x 16, w = sqrt(lambda_k) * xi (no contraction)
-    for (int e = tid; e < RL_BM * RL_BK; e += RL_THREADS) {
-      const int rb = e / RL_BK, kk = e % RL_BK;
+  double rw[NWE], rp[NPE];
+  auto load_block = [&](int k0) {
+#pragma unroll
+    for (int u = 0; u < NWE; ++u) {  // W tile: 64 x 16, w = sqrt(lambda_k) * xi (no contraction)
+      const int e = tid + u * RL_THREADS, rb = e / RL_BK, kk = e % RL_BK;
       const int64_t b = b0 + rb;
       const int k = k0 + kk;
-      double v = 0.0;
-      if (b < prm.B && k < prm.K_use) v = __dmul_rn(prm.sqrt_lam[k], prm.xi[b * prm.ld + k]);
-      sW[rb * RL_WLD + kk] = v;
+      rw[u] = (b < prm.B && k < prm.K_use) ? __dmul_rn(prm.sqrt_lam[k], prm.xi[b * prm.ld + k]) : 0.0;
     }
-    // Phi tile: 16 x 128 (coalesced along points)
-    for (int e = tid; e < RL_BK * RL_BN; e += RL_THREADS) {
-      const int kk = e / RL_BN, ii = e % RL_BN;
+#pragma unroll
+    for (int u = 0; u < NPE; ++u) {  // Phi tile: 16 x 128 (coalesced along points)
+      const int e = tid + u * RL_THREADS, kk = e / RL_BN, ii = e % RL_BN;
       const int k = k0 + kk, i = i0 + ii;
-      sP[kk * RL_PLD + ii] = (k < prm.K_use && i < prm.n_nodes)
-                                 ? prm.phi[static_cast<size_t>(k) * prm.n_nodes + i]
-                                 : 0.0;
+      rp[u] = (k < prm.K_use && i < prm.n_nodes) ? prm.phi[static_cast<size_t>(k) * prm.n_nodes + i] : 0.0;
     }
-    __syncthreads();
+  };
+  auto store_block = [&](int stage) {
+    double* sW = rl_smem + stage * RL_STAGE;
+    double* sP = sW + RL_BM * RL_WLD;
+#pragma unroll
+    for (int u = 0; u < NWE; ++u) {
+      const int e = tid + u * RL_THREADS;
+      sW[(e / RL_BK) * RL_WLD + e % RL_BK] = rw[u];
+    }
+#pragma unroll
+    for (int u = 0; u < NPE; ++u) {
+      const int e = tid + u * RL_THREADS;
+      sP[(e / RL_BN) * RL_PLD + e % RL_BN] = rp[u];
+    }
+  };
+  load_block(0);
+  store_block(0);
+  __syncthreads();
+  int stage = 0;
+  for (int k0 = 0; k0 < prm.K_use; k0 += RL_BK, stage ^= 1) {
+    const bool more = k0 + RL_BK < prm.K_use;
+    if (more) load_block(k0 + RL_BK);
+    const double* sW = rl_smem + stage * RL_STAGE;
+    const double* sP = sW + RL_BM * RL_WLD;
 #pragma unroll
     for (int ks = 0; ks < RL_BK; ks += 4) {
       double af[4], bf[4];
@@ -90,6 +118,8 @@ static __global__ void __launch_bounds__(RL_THREADS) realise_kernel(const Realis
 #pragma unroll
         for (int c = 0; c < 4; ++c) dmma_8x8x4(acc[a][c][0], acc[a][c][1], af[a], bf[c]);
     }
+    if (more) store_block(stage ^ 1);  // last read two blocks ago, before the previous barrier
+    __syncthreads();
   }
   // epilogue: C (8x8): row = lane/4, cols = 2*(lane%4) + {0,1}
 #pragma unroll

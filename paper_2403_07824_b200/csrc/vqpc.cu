@@ -344,10 +344,12 @@ void run_realise(vqpc_ctx* c, const double* d_xi, int64_t B, int64_t ld, int K_u
   RealiseParams prm{d_xi, ld, B, c->sqrt_lam.p, c->phi.p, c->pb.n_nodes, K_use, d_kappa, ldk, d_flag};
   dim3 grid(static_cast<unsigned>(ceil_div(c->pb.n_nodes, RL_BN)), static_cast<unsigned>(ceil_div(B, RL_BM)));
   Timed tm(c, VQPC_K_REALISE);
-  if (c->exact)  // reference-order mode: the reference's k-outer AXPY on the CUDA cores
+  if (c->exact) {  // reference-order mode: the reference's k-outer AXPY on the CUDA cores
     realise_exact_kernel<<<grid, RL_THREADS, 0, c->stream>>>(prm);
-  else
-    realise_kernel<<<grid, RL_THREADS, 0, c->stream>>>(prm);
+  } else {
+    CK(cudaFuncSetAttribute(realise_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(RL_SMEM)));
+    realise_kernel<<<grid, RL_THREADS, RL_SMEM, c->stream>>>(prm);
+  }
   launch_check(c);
 }
 
@@ -1041,9 +1043,9 @@ void setup_amg(vqpc_ctx* c, const double* d_kc, int64_t ldk, int P) {
   // pack: ints (slice offsets + columns) and doubles (values, inverse diagonals, dense L)
   std::vector<int> hi;
   std::vector<double> hd;
-  struct EllOff { size_t soff, col, val, rlen; };
+  struct EllOff { size_t row, rec; };
   auto pack_ell = [&](const amg::Csr& M) {
-    EllOff o{hi.size(), 0, 0, 0};
+    EllOff o{};
     const int ns = (M.rows + 31) / 32;
     std::vector<int> soff(ns + 1, 0);
     for (int s = 0; s < ns; ++s) {
@@ -1051,18 +1053,25 @@ void setup_amg(vqpc_ctx* c, const double* d_kc, int64_t ldk, int P) {
       for (int i = 32 * s; i < std::min(M.rows, 32 * s + 32); ++i) w = std::max(w, M.ptr[i + 1] - M.ptr[i]);
       soff[s + 1] = soff[s] + 32 * w;
     }
-    hi.insert(hi.end(), soff.begin(), soff.end());
-    o.rlen = hi.size();
-    for (int i = 0; i < M.rows; ++i) hi.push_back(M.ptr[i + 1] - M.ptr[i]);
-    o.col = hi.size();
-    o.val = hd.size();
-    hi.resize(hi.size() + soff[ns], -1);
-    hd.resize(hd.size() + soff[ns], 0.0);
+    if (hi.size() & 1) hi.push_back(0);  // int2 alignment of the per-row {first record, length}
+    o.row = hi.size();
+    for (int i = 0; i < M.rows; ++i) {
+      hi.push_back(soff[i >> 5] + (i & 31));
+      hi.push_back(M.ptr[i + 1] - M.ptr[i]);
+    }
+    if (hd.size() & 1) hd.push_back(0.0);  // 16-byte alignment of the records
+    o.rec = hd.size();
+    hd.resize(hd.size() + 2 * static_cast<size_t>(soff[ns]), 0.0);
+    for (size_t e = 0; e < static_cast<size_t>(soff[ns]); ++e) {  // padding records: value 0, column -1
+      const long long pad = -1;
+      std::memcpy(&hd[o.rec + 2 * e + 1], &pad, sizeof(double));
+    }
     for (int i = 0; i < M.rows; ++i)
       for (int k = 0; k < M.ptr[i + 1] - M.ptr[i]; ++k) {
         const size_t e = soff[i >> 5] + 32 * static_cast<size_t>(k) + (i & 31);
-        hi[o.col + e] = M.idx[M.ptr[i] + k];
-        hd[o.val + e] = M.val[M.ptr[i] + k];
+        hd[o.rec + 2 * e] = M.val[M.ptr[i] + k];
+        const long long col = M.idx[M.ptr[i] + k];
+        std::memcpy(&hd[o.rec + 2 * e + 1], &col, sizeof(double));
       }
     return o;
   };
@@ -1120,7 +1129,8 @@ void setup_amg(vqpc_ctx* c, const double* d_kc, int64_t ldk, int P) {
   h2d(c, c->amg_i.p, hi.data(), hi.size());
   h2d(c, c->amg_d.p, hd.data(), hd.size());
   auto ell_ptr = [&](const EllOff& o, int rows, int cols) {
-    return AmgEll{c->amg_i.p + o.soff, c->amg_i.p + o.col, c->amg_d.p + o.val, c->amg_i.p + o.rlen, rows, cols};
+    return AmgEll{reinterpret_cast<const int2*>(c->amg_i.p + o.row), reinterpret_cast<const double2*>(c->amg_d.p + o.rec),
+                  rows, cols};
   };
   for (int p = 0; p < P; ++p) {
     for (int l = 0; l < hh[p].nlev; ++l) {
