@@ -33,6 +33,10 @@ constexpr int AMG_MAXDENSE = 1024;  // coarsest dense solve size (shared-memory 
 #define AMG_ROWU 1                   // rows per thread interleaved in the V-cycle passes (A/B builds)
 #endif
 constexpr int kAmgRowU = AMG_ROWU;
+#ifndef AMG_PCGU
+#define AMG_PCGU 1                   // rows per thread interleaved in the two PCG passes (A/B builds)
+#endif
+constexpr int kAmgPcgU = AMG_PCGU;
 #ifndef AMG_MINB
 #define AMG_MINB 3                   // resident CTAs per SM the register budget targets (3: +12 % over 2, r02f A/B)
 #endif
@@ -534,6 +538,7 @@ __global__ void __launch_bounds__(AMG_T, AMG_MINB) pcgamg2d_kernel(const PcgAmgP
       const bool first = j == 1;
 #pragma unroll
       for (int s = 0; s < S; ++s) part[s] = 0.0;
+#pragma unroll kAmgPcgU
       for (int i = t; i < n; i += AMG_T) {
         const int ix = i % m, iy = i / m;
         const bool hs = iy > 0, hw = ix > 0, he = ix < m - 1, hn = iy < m - 1;
@@ -572,6 +577,7 @@ __global__ void __launch_bounds__(AMG_T, AMG_MINB) pcgamg2d_kernel(const PcgAmgP
       double* Xn = Xb[xc ^ 1];
 #pragma unroll
       for (int s = 0; s < S; ++s) part[s] = 0.0;
+#pragma unroll kAmgPcgU
       for (int i = t; i < n; i += AMG_T) {
         const int ix = i % m, iy = i / m;
         const bool hs = iy > 0, hw = ix > 0, he = ix < m - 1, hn = iy < m - 1;
