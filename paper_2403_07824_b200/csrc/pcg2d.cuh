@@ -300,8 +300,6 @@ struct Pcg2dParams {
   double* x_out;            // nullable, natural interior order
   int exact;                // 1: dot products summed serially in natural order (reference bits)
   const int* gmap;          // per wavefront address: level | (iy << 16)
-  const int2* groups;       // pair kernel: (first entry in perm, count <= 2), one label each
-  const int* ngroups;
   const double* bvec;       // per wavefront address: b_i = area_sum_i / 3 when the mesh's b is not
                             // uniform (h = 1/r inexact: every triangle area rounds differently); null:
                             // b is the same for every node (r a power of two, e.g. C4) and read once

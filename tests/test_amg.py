@@ -177,7 +177,7 @@ def test_amg_kind_without_device():
 @pytest.mark.gpu
 def test_gpu_amg_paper_size_mesh():
     """The paper's problem size (n = 99,681 unknowns) on the structured
-    mesh r = 317 (99,856 unknowns; beyond the IC(0) kind's r <= 257): the SA-AMG
+    mesh r = 317 (99,856 unknowns; beyond the cholesky kind's r <= 257): the SA-AMG
     kind runs it, bit-identical to the oracle in reference-order mode."""
     name = "C4amg317"
     CONFIGS.setdefault(name, campaign.scaled(campaign.CONFIGS["C4amg"], mesh_resolution=317, name=name))

@@ -1,8 +1,8 @@
-"""A/B one build of libvqpc.so under two environment settings (e.g. VQPC_P2_PAIR=0
-vs 1) on one config: device-campaign time and whether every per-sample record is
+"""A/B one build of libvqpc.so under two environment settings (e.g. VQPC_MAX_GROUPS=148
+vs 296) on one config: device-campaign time and whether every per-sample record is
 bit-identical.
 
-usage: python tools/ab_env.py C4 2048 VQPC_P2_PAIR=0 VQPC_P2_PAIR=1 [reps] [exact]
+usage: python tools/ab_env.py C4 2048 VQPC_MAX_GROUPS=148 VQPC_MAX_GROUPS=296 [reps] [exact]
 """
 import os
 import subprocess
