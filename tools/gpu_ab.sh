@@ -1,5 +1,6 @@
-O=gpurun_out/r02o
+O=gpurun_out/r02q
 mkdir -p $O
-VQPC_LIB=ab_libs/libvqpc_base.so timeout 900 python bench.py --config C4amg --steps 2 --warmup 2 --no-cpu --e2e-steps 1 > $O/bench_c4amg_baselib.json 2> $O/bench_c4amg_baselib.err
-tail -c 300 $O/bench_c4amg_baselib.json
-timeout 900 python bench.py --config C4amg --steps 2 --warmup 2 --no-cpu --e2e-steps 1 > $O/bench_c4amg_newlib.json 2> $O/bench_c4amg_newlib.err
+for v in pf1 pf2 pf3 pf2l1; do
+  timeout 900 python tools/ab_libs.py C4amg 2664 ab_libs/libvqpc_pf0.so ab_libs/libvqpc_$v.so 1 > $O/ab_amg2_$v.log 2>&1
+  tail -n 2 $O/ab_amg2_$v.log | head -1; tail -n 1 $O/ab_amg2_$v.log
+done
