@@ -30,6 +30,11 @@
 
 namespace vqpc {
 
+#ifndef PC_PF
+#define PC_PF 1   // batches ahead the vector passes pull their streamed operands into L2 (0: off)
+#endif
+__device__ __forceinline__ void pc_prefetch(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 constexpr int PC_T = 256;     // threads per CTA
 constexpr int PC_BS = 32;     // rows per block of the triangular solves
 constexpr int PC_RING = 1024; // y / w ring (rows)
@@ -626,6 +631,16 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
         // per-row operations and accumulation order): 8 warps per SM need the MLP
         for (int k0 = t; k0 < n; k0 += PC_U * PC_T) {
           double zv[PC_U], pv[PC_U];
+          if (PC_PF > 0) {
+#pragma unroll
+            for (int u = 0; u < PC_U; ++u) {
+              const int kp = k0 + (PC_PF * PC_U + u) * PC_T;
+              if (kp < n) {
+                pc_prefetch(Z + kp);
+                if (j != 1) pc_prefetch(P + kp);
+              }
+            }
+          }
 #pragma unroll
           for (int u = 0; u < PC_U; ++u) {
             const int k = k0 + u * PC_T;
@@ -649,6 +664,21 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
         double* AP = vec(s, VAP);
         for (int k0 = t; k0 < n; k0 += PC_U2 * PC_T) {
           double ap[PC_U2], pk[PC_U2];
+          if (PC_PF > 0) {
+#pragma unroll
+            for (int u = 0; u < PC_U2; ++u) {
+              const int kp = k0 + (PC_PF * PC_U2 + u) * PC_T;
+              if (kp < n) {
+                pc_prefetch(lay.nbr + kp);
+                pc_prefetch(P + kp);
+                pc_prefetch(vec(s, VS) + kp);
+                pc_prefetch(vec(s, VW) + kp);
+                pc_prefetch(vec(s, VD) + kp);
+                pc_prefetch(vec(s, VE) + kp);
+                pc_prefetch(vec(s, VN) + kp);
+              }
+            }
+          }
 #pragma unroll
           for (int u = 0; u < PC_U2; ++u) {
             const int k = k0 + u * PC_T;
@@ -699,6 +729,25 @@ __global__ void __launch_bounds__(PC_T, 1) pcgchol2d_kernel(const PcholParams pr
         auto xnew = [&](int i) { return __dadd_rn(Xo[i], __dmul_rn(a, P[i])); };
         for (int k0 = t; k0 < n; k0 += PC_U2 * PC_T) {
           double rt[PC_U2];
+          if (PC_PF > 0) {
+#pragma unroll
+            for (int u = 0; u < PC_U2; ++u) {
+              const int kp = k0 + (PC_PF * PC_U2 + u) * PC_T;
+              if (kp < n) {
+                pc_prefetch(lay.nbr + kp);
+                pc_prefetch(Xo + kp);
+                pc_prefetch(P + kp);
+                pc_prefetch(AP + kp);
+                pc_prefetch(R + kp);
+                pc_prefetch(vec(s, VB) + kp);
+                pc_prefetch(vec(s, VS) + kp);
+                pc_prefetch(vec(s, VW) + kp);
+                pc_prefetch(vec(s, VD) + kp);
+                pc_prefetch(vec(s, VE) + kp);
+                pc_prefetch(vec(s, VN) + kp);
+              }
+            }
+          }
 #pragma unroll
           for (int u = 0; u < PC_U2; ++u) {
             const int k = k0 + u * PC_T;

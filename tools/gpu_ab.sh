@@ -1,6 +1,6 @@
 O=gpurun_out/r02q
 mkdir -p $O
-timeout 1200 python -m pytest tests/test_amg.py tests/test_ideal_sweep.py tests/test_integration.py -q -m gpu > $O/amg_tests.log 2>&1
-tail -n 2 $O/amg_tests.log
-timeout 1200 python bench.py --config C4amg --steps 3 --warmup 3 > $O/bench_c4amg.json 2> $O/bench_c4amg.err
-tail -c 200 $O/bench_c4amg.json
+for v in c1 c2; do
+  timeout 900 python tools/ab_libs.py C4chol 2368 ab_libs/libvqpc_c0.so ab_libs/libvqpc_$v.so 1 > $O/ab_chol_$v.log 2>&1
+  tail -n 2 $O/ab_chol_$v.log | head -1; tail -n 1 $O/ab_chol_$v.log
+done
