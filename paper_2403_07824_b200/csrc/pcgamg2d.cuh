@@ -43,6 +43,10 @@ __device__ __forceinline__ void amg_prefetch(const void* p) { asm volatile("pref
 #else
 __device__ __forceinline__ void amg_prefetch(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 #endif
+#ifndef AMG_ELLU
+#define AMG_ELLU 4                   // entries of an ELL row whose loads issue together (A and P^T rows; A/B builds)
+#endif
+constexpr int kAmgEllU = AMG_ELLU;
 #ifndef AMG_PCGU
 #define AMG_PCGU 1                   // rows per thread interleaved in the two PCG passes (A/B builds)
 #endif
@@ -152,7 +156,7 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
       } else {
       const int w = rw.y;
       int e = rw.x;
-      #pragma unroll 4
+      #pragma unroll kAmgEllU
       for (int k = 0; k < w; ++k, e += 32) {
         const double2 rc = __ldg(L.A.rec + e);
         const int c = ell_col(rc);
@@ -179,7 +183,7 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
       for (int s = 0; s < S; ++s) acc[s] = 0.0;
       const int w = rw.y;
       int e = rw.x;
-      #pragma unroll 4
+      #pragma unroll kAmgEllU
       for (int k = 0; k < w; ++k, e += 32) {
         const double2 rc = __ldg(L.Pt.rec + e);
         const int q = ell_col(rc);
@@ -249,7 +253,7 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
         const int2 rw = ell_row(L.A, i);
         const int w = rw.y;
         int e = rw.x;
-        #pragma unroll 4
+        #pragma unroll kAmgEllU
         for (int k = 0; k < w; ++k, e += 32) {
           const double2 rc = __ldg(L.A.rec + e);
           const int c = ell_col(rc);
@@ -343,7 +347,7 @@ __device__ void amg_vcycle(const AmgHierD& H, double omega, const double* r0, do
       } else {
       const int w = rw.y;
       int e = rw.x;
-      #pragma unroll 4
+      #pragma unroll kAmgEllU
       for (int k = 0; k < w; ++k, e += 32) {
         const double2 rc = __ldg(L.A.rec + e);
         const int c = ell_col(rc);
