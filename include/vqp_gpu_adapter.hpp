@@ -78,6 +78,12 @@ class Context {
   Context(const CampaignArtifacts& art, const GpuOptions& opt, int precond) {
     const Codebook& cb = art.codebook;
     const KLBasis& basis = art.basis;
+    // import_mesh (fem.cpp:83-114) leaves resolution = 0: the device kernels are written for
+    // the structured mesh of make_mesh (fem.cpp:53-81) and refuse an unstructured one
+    if (opt.dim == 2 && opt.size <= 0 && art.mesh.resolution <= 0)
+      throw Error("invalid-config",
+                  "invalid-config: the mesh was imported (TriMesh::resolution == 0); the GPU path needs the "
+                  "structured r x r mesh of make_mesh (any r with the amg kind, r <= 513 ic0, r <= 257 cholesky)");
     vqpc_problem pb{};
     pb.dim = opt.dim;
     pb.size = opt.size > 0 ? opt.size : art.mesh.resolution;
