@@ -218,6 +218,18 @@ __device__ __forceinline__ int wf_size(int l, int m) { return l < m ? l + 1 : 2 
 __device__ __forceinline__ int wf_dw(int l, int m) { return wf_size(l - 1, m) + lvl_lo(l - 1, m) - lvl_lo(l, m); }
 __device__ __forceinline__ int wf_de(int l, int m) { return wf_size(l, m) + lvl_lo(l, m) - lvl_lo(l + 1, m); }
 
+// level of a wavefront address, tracked instead of looked up: {level, its first address, its size}
+struct LvlCursor {
+  int l, off, sz;
+};
+__device__ __forceinline__ void lvl_advance(LvlCursor& c, int a, int m) {
+  while (a >= c.off + c.sz) {
+    c.off += c.sz;
+    ++c.l;
+    c.sz = wf_size(c.l, m);
+  }
+}
+
 #ifdef VQPC_PHASE_TIMING
 __device__ unsigned long long g_pcg2d_phase[4];  // cycles: setup, sweeps, P1, P2 (CTA thread 0)
 #define P2_TIC(v) const long long v = clock64()
@@ -324,7 +336,7 @@ constexpr int P2_XCH = 4;      // exchange rings: p (or p_new), x_new, aW, aS; 4
 // dynamic shared memory of pcg2d_kernel<MC, TT>: the larger of the sweeps' ring and the flat passes' slots
 constexpr size_t p2_dsmem(int tt) {
   const size_t ring = sizeof(double) * P2_DEPTH * P2_NOPS * tt;
-  const size_t flat = sizeof(double) * (P2_RSLOT * P2_RAW + 4 * P2_XCH) * tt + sizeof(int) * P2_RSLOT * tt;
+  const size_t flat = sizeof(double) * (P2_RSLOT * P2_RAW + 4 * P2_XCH) * tt;
   return ring > flat ? ring : flat;
 }
 
@@ -415,6 +427,8 @@ __global__ void __launch_bounds__(TT, TT == TT ? 2 : 1) pcg2d_kernel(const Pcg2d
   }
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   for (int l = t; l < g.L; l += TT) lvl_dd[l] = make_int2(l > 0 ? wf_dw(l, g.m) : 0, l + 1 < g.L ? wf_de(l, g.m) : 0);
+  LvlCursor lc0{0, 0, 1};  // level of wavefront address t (the first chunk of the flat passes)
+  if (t < g.n) lvl_advance(lc0, t, g.m);
   __syncthreads();
   const int n = g.n;
   double* base = prm.work + static_cast<size_t>(blockIdx.x) * P2_WORK * n;
@@ -616,7 +630,6 @@ __global__ void __launch_bounds__(TT, TT == TT ? 2 : 1) pcg2d_kernel(const Pcg2d
         const int NC = (n + TT - 1) / TT;
         double* raw = dsm;                                   // [P2_RSLOT][P2_RAW][TT]
         double* xch = dsm + P2_RSLOT * P2_RAW * TT;        // [P2_XCH][4][TT]
-        int* rawi = reinterpret_cast<int*>(xch + 4 * P2_XCH * TT);  // [P2_RSLOT][TT]
         auto RAW = [&](int k, int v) -> double* { return raw + ((static_cast<unsigned>(k) % P2_RSLOT) * P2_RAW + v) * TT + t; };
         // chunk slot (q >> 8) & 3, column q & 255: together q & 1023
         auto XCH = [&](int x, int q) -> double& { return xch[x * 4 * TT + (q & (4 * TT - 1))]; };
@@ -630,14 +643,16 @@ __global__ void __launch_bounds__(TT, TT == TT ? 2 : 1) pcg2d_kernel(const Pcg2d
             cp_async8p(RAW(k, 3), As + a, pol_str);
             cp_async8p(RAW(k, 4), Aw + a, pol_str);
             cp_async8p(RAW(k, 5), Ad + a, pol_str);
-            cp_async4(rawi + (static_cast<unsigned>(k) % P2_RSLOT) * TT + t, prm.gmap + a);
           }
           cp_commit();
         };
-        // neighbour addresses of wavefront address a (level l, row iy); -1 off the mesh
+        // neighbour addresses of wavefront address a (level l, row iy); -1 off the mesh. The
+        // level of a thread's address is tracked by a cursor {level, its offset, its size} that
+        // advances with the address (one or two levels per chunk away from the corners), so the
+        // flat passes read no per-address map.
         struct Nb { int s, w, e, nn, ix, iy; };
-        auto nbrs = [&](int a, int lv) {
-          const int l = lv & 0xffff, iy = lv >> 16, ix = l - iy;
+        auto nbrs = [&](int a, const LvlCursor& c) {
+          const int l = c.l, iy = lvl_lo(l, g.m) + (a - c.off), ix = l - iy;
           Nb b;
           const int2 dd = lvl_dd[l];
           const int dw = dd.x, de = dd.y;
@@ -654,10 +669,9 @@ __global__ void __launch_bounds__(TT, TT == TT ? 2 : 1) pcg2d_kernel(const Pcg2d
         {
           for (int k = 0; k < P2_SD; ++k) flat_issue(k, Z, first ? nullptr : Po, nullptr);
           double cs = 0.0, cw = 0.0, cd = 0.0;
-          int clv = 0;
+          LvlCursor lc = lc0;  // level of address (k - 1) TT + t
           for (int k = 0; k <= NC; ++k) {
             const double ps = cs, pw = cw, pd = cd;
-            const int plv = clv;
             if (k < NC) {
               cp_wait<P2_SD - 1>();
               const int a = k * TT + t;
@@ -667,7 +681,6 @@ __global__ void __launch_bounds__(TT, TT == TT ? 2 : 1) pcg2d_kernel(const Pcg2d
                 cs = *RAW(k, 3);
                 cw = *RAW(k, 4);
                 cd = *RAW(k, 5);
-                clv = rawi[(static_cast<unsigned>(k) % P2_RSLOT) * TT + t];
                 XCH(0, a) = pcv;
                 XCH(2, a) = cw;
                 XCH(3, a) = cs;
@@ -678,7 +691,8 @@ __global__ void __launch_bounds__(TT, TT == TT ? 2 : 1) pcg2d_kernel(const Pcg2d
             __syncthreads();
             const int a = (k - 1) * TT + t;
             if (k >= 1 && a < n) {
-              const Nb b = nbrs(a, plv);
+              lvl_advance(lc, a, g.m);
+              const Nb b = nbrs(a, lc);
               const double pcv = XCH(0, a);
               const double ap = row_apply(ps, pw, pd, xv(2, b.e), xv(3, b.nn), xv(0, b.s), xv(0, b.w), pcv,
                                           xv(0, b.e), xv(0, b.nn));
@@ -706,11 +720,10 @@ __global__ void __launch_bounds__(TT, TT == TT ? 2 : 1) pcg2d_kernel(const Pcg2d
         {
           for (int k = 0; k < P2_SD; ++k) flat_issue(k, Pv, Xo, Rv);
           double cs = 0.0, cw = 0.0, cd = 0.0, cr = 0.0;
-          int clv = 0;
+          LvlCursor lc = lc0;  // level of address (k - 1) TT + t
           double cb = bval;  // b of this thread's address in the chunk being loaded
           for (int k = 0; k <= NC; ++k) {
             const double ps = cs, pw = cw, pd = cd, pr = cr, pb = cb;
-            const int plv = clv;
             if (k < NC) {
               cp_wait<P2_SD - 1>();
               const int a = k * TT + t;
@@ -722,7 +735,6 @@ __global__ void __launch_bounds__(TT, TT == TT ? 2 : 1) pcg2d_kernel(const Pcg2d
                 cs = *RAW(k, 3);
                 cw = *RAW(k, 4);
                 cd = *RAW(k, 5);
-                clv = rawi[(static_cast<unsigned>(k) % P2_RSLOT) * TT + t];
                 XCH(0, a) = pvv;
                 XCH(1, a) = xn;
                 XCH(2, a) = cw;
@@ -734,7 +746,8 @@ __global__ void __launch_bounds__(TT, TT == TT ? 2 : 1) pcg2d_kernel(const Pcg2d
             __syncthreads();
             const int a = (k - 1) * TT + t;
             if (k >= 1 && a < n) {
-              const Nb b = nbrs(a, plv);
+              lvl_advance(lc, a, g.m);
+              const Nb b = nbrs(a, lc);
               const double aE = xv(2, b.e), aN = xv(3, b.nn);
               const double ap = row_apply(ps, pw, pd, aE, aN, xv(0, b.s), xv(0, b.w), XCH(0, a), xv(0, b.e),
                                           xv(0, b.nn));
