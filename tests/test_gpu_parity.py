@@ -414,7 +414,7 @@ def test_1d_tiny_meshes(N):
         assert out["iterations"] == it[i] and out["rel"] == rel[i] and np.array_equal(out["x"], x[i]), i
 
 
-@pytest.mark.parametrize("r", [4, 17, 100, 257, 300, 513])
+@pytest.mark.parametrize("r", [4, 17, 100, 257, 258, 300, 513])
 def test_2d_other_mesh_sizes_exact_mode(r):
     """2-D meshes other than C4's (generic kernel instantiation, odd and tiny m,
     the largest mesh of the 256-thread kernel, m = 256 interior nodes per row, and
