@@ -329,7 +329,11 @@ constexpr int P2_NOPS = 6;   // operands per node in the ring
 // a raw slot only it reads, and publishes the vector values its neighbours need
 // into 4-slot exchange rings (a node's neighbours lie in chunks k-1..k+1 since a
 // level holds <= TT nodes). One barrier per chunk.
+#ifndef P2_SD_OVERRIDE
 constexpr int P2_SD = 3;       // chunks in flight
+#else
+constexpr int P2_SD = P2_SD_OVERRIDE;
+#endif
 constexpr int P2_RSLOT = P2_SD + 1;  // raw slots: the slot refilled in step k is the one read in step k-1
 constexpr int P2_RAW = 6;      // raw double vectors per address
 constexpr int P2_XCH = 4;      // exchange rings: p (or p_new), x_new, aW, aS; 4 chunk slots each (k-2..k+1 live)
