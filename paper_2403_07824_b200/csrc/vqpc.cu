@@ -529,7 +529,10 @@ void run_pcgamg2d(vqpc_ctx* c, const double* d_kappa, int64_t ldk, const uint8_t
                   const int32_t* d_labels, int64_t B, int64_t out_base, double eps, int max_iter, const int32_t* d_mia,
                   int32_t* d_iters, double* d_rel, uint8_t* d_status, double* d_x, int64_t solve_limit) {
   const int P = c->pb.P;
-  int S = 1;  // samples per CTA (VQPC_AMG_S overrides: 1, 2, 4, 8; 1 measured fastest)
+  // samples per CTA (same label: the centroid's hierarchy is loaded once for all of them).
+  // VQPC_AMG_S overrides: 1, 2, 4, 8. On 5,328 C4amg samples (final round-2 kernel) 2 gives
+  // 1,262 samples/s, 1 gives 1,134, 4 gives 952 (profiles/r02u_ab_amg_s*.log); records identical
+  int S = 2;
   if (const char* e = getenv("VQPC_AMG_S")) S = atoi(e);
   S = S >= 8 ? 8 : S >= 4 ? 4 : S >= 2 ? 2 : 1;
   c->ch_perm.ensure(B);
